@@ -1,0 +1,150 @@
+/*
+ * pastis_sw.h -- C ABI of the B200-native batched Smith-Waterman aligner
+ * (libpastis_sw.so, built from paper_2303_01845_b200/csrc/).
+ *
+ * The reference (/root/reference/pkg/src/pastislite, pure Python) has no FFI;
+ * its drop-in seam is the Python API of pastislite.align.  Each entry point
+ * below replaces one piece of that API; the Python mirror in
+ * paper_2303_01845_b200/align.py calls these through ctypes.
+ *
+ *   sw_align_batch        replaces align.align_batch's per-pair loop
+ *                         (align.py:223-246 -> _smith_waterman_timed
+ *                         align.py:79-181) for a whole batch at once.
+ *   sw_align_batch_multi  replaces AlignEngine's process-pool lanes
+ *                         (align.py:299-347, _chunk align.py:265-269) with a
+ *                         cell-balanced shard over several GPUs.
+ *   sw_align_batch_device same as sw_align_batch on device-resident buffers.
+ *   sw_result_t           AlignmentResult (align.py:55-67) minus `cells`
+ *                         (= a_len*b_len, computed by the caller) plus a
+ *                         per-pair status that maps to AlignmentError
+ *                         (align.py:33-34, raised at align.py:81-82).
+ *   sw_params_t           AlignParams (align.py:37-52) gap_open, gap_extend,
+ *                         matrix (25x25, alphabet order of alphabet.py:8).
+ *
+ * Sequences are passed as RAW BYTES (what the reference receives as str):
+ * the byte->residue mapping of align.py:27-30 (unknown -> 'X') is applied on
+ * the device, and `matches` compares raw bytes exactly like align.py:142.
+ *
+ * Error convention: functions return 0 on success and a negative SW_E* code
+ * on a call-level failure; sw_last_error() then describes it (thread-local).
+ * Per-pair failures never fail the call: they are reported in
+ * sw_result_t.status (align_batch's per-pair isolation, align.py:235-241).
+ */
+#ifndef PASTIS_SW_H
+#define PASTIS_SW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SW_ABI_VERSION 1
+
+/* call-level return codes */
+#define SW_OK 0
+#define SW_EINVAL (-1)   /* bad arguments / parameters outside the supported domain */
+#define SW_ECUDA (-2)    /* CUDA runtime error (no device, OOM, launch failure) */
+#define SW_EINTERNAL (-3)
+
+/* per-pair status codes (sw_result_t.status) */
+#define SW_STATUS_OK 0
+#define SW_STATUS_EMPTY 1     /* empty sequence: AlignmentError (align.py:81-82) */
+#define SW_STATUS_INTERNAL 2  /* traceback lost: AssertionError (align.py:150) */
+
+typedef struct sw_pair_t { /* one candidate pair; a = rows, b = columns */
+  uint64_t a_off;          /* byte offset of sequence a in the arena */
+  uint64_t b_off;          /* byte offset of sequence b in the arena */
+  uint32_t a_len;
+  uint32_t b_len;
+} sw_pair_t;               /* 24 bytes */
+
+typedef struct sw_params_t {
+  int32_t gap_open;        /* first gap residue costs gap_open */
+  int32_t gap_extend;      /* each further residue costs gap_extend */
+  int32_t matrix[25 * 25]; /* symmetric, row-major, alphabet ARNDCQEGHILKMFPSTWYVBZXU* */
+} sw_params_t;
+/* Supported domain (checked, SW_EINVAL otherwise): 0 <= gap_extend <=
+ * gap_open <= 16383 and every matrix entry in [-127, 127].  BLOSUM62
+ * (entries -4..11) with 11/1 or 11/2 is well inside it. */
+
+typedef struct sw_result_t { /* AlignmentResult fields, 0-based inclusive spans */
+  int32_t score;
+  int32_t i_begin, i_end;  /* -1 for the empty (score 0) alignment */
+  int32_t j_begin, j_end;
+  int32_t matches;         /* identical aligned residue pairs */
+  int32_t aln_len;         /* alignment columns including gaps */
+  int32_t status;          /* SW_STATUS_* */
+} sw_result_t;             /* 32 bytes */
+
+typedef struct sw_timing_t { /* filled when non-NULL; device times from CUDA events */
+  double forward_ms;       /* K1: forward score + end cell (paper's "forward scoring time") */
+  double reverse_ms;       /* K2: reverse pass -> start box */
+  double traceback_ms;     /* K3 + walk: box recompute with direction codes + traceback */
+  double kernel_ms;        /* all device work of the call (encode .. walk) */
+  double h2d_ms;           /* host->device copies (host-buffer entry points only) */
+  double d2h_ms;           /* device->host copy of the results */
+  double total_ms;         /* wall time of the call */
+  uint64_t cells;          /* sum of a_len*b_len over non-empty pairs */
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  uint32_t launches;       /* kernels launched by the call */
+  uint32_t wide_pairs;     /* pairs that needed the 32-bit-wide score path */
+  uint64_t box_cells;      /* cells recomputed by K3 (sum of box areas) */
+  uint64_t rev_cells;      /* cells scored by K2 */
+} sw_timing_t;
+
+/* Number of visible CUDA devices (0 when none). */
+int sw_get_device_count(void);
+
+/* Human-readable description of the last failure on this thread. */
+const char *sw_last_error(void);
+
+/* ABI version of the loaded library (== SW_ABI_VERSION). */
+int sw_abi_version(void);
+
+/* Align n_pairs pairs whose bytes live in a HOST arena; results in HOST
+ * memory, in input order.  Copies in, runs forward/reverse/traceback
+ * kernels on `device`, copies out.  Synchronous.  Pinned host buffers give
+ * the fastest copies but any host memory works. */
+int sw_align_batch(int device, const uint8_t *arena, uint64_t arena_bytes,
+                   const sw_pair_t *pairs, uint64_t n_pairs, const sw_params_t *params,
+                   sw_result_t *out, sw_timing_t *timing);
+
+/* Same on DEVICE-resident buffers (arena, pairs and out all on `device`).
+ * `stream` is a cudaStream_t (NULL = the library's own stream).  Returns
+ * after the work completes. */
+int sw_align_batch_device(int device, const uint8_t *d_arena, uint64_t arena_bytes,
+                          const sw_pair_t *d_pairs, uint64_t n_pairs,
+                          const sw_params_t *params, sw_result_t *d_out, void *stream,
+                          sw_timing_t *timing);
+
+/* Shard a HOST batch over n_devices GPUs by cell count (|a|*|b|, greedy
+ * least-loaded), run every shard concurrently (one host thread per GPU),
+ * gather results into `out` in input order.  per_device_timing may be NULL
+ * or point to n_devices entries. */
+int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena,
+                         uint64_t arena_bytes, const sw_pair_t *pairs, uint64_t n_pairs,
+                         const sw_params_t *params, sw_result_t *out,
+                         sw_timing_t *per_device_timing);
+
+/* Cell-balanced partition used by sw_align_batch_multi, exposed for the host
+ * driver and its tests: writes shard[k] in [0, n_shards) for every pair
+ * (LPT: pairs in descending a_len*b_len order go to the least-loaded shard).
+ * load[s] (may be NULL) receives the cell total of shard s. */
+int sw_partition_pairs(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards,
+                       int32_t *shard, uint64_t *load);
+
+/* Release cached device buffers of `device` (-1 = all devices). */
+void sw_release(int device);
+
+/* Page-locked host memory for arenas / pair tables / results (fast copies).
+ * Returns NULL on failure (sw_last_error). */
+void *sw_host_alloc(uint64_t bytes);
+void sw_host_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PASTIS_SW_H */

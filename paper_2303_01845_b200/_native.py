@@ -1,0 +1,202 @@
+"""ctypes binding of libpastis_sw.so (C ABI: include/pastis_sw.h).
+
+There is no CPU fallback: if the library or a GPU is missing, every compute
+entry point raises.  The library is built in-tree by __graft_entry__.build()
+(or `python -m paper_2303_01845_b200.build`).
+"""
+
+import ctypes
+import os
+import threading
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpastis_sw.so")
+
+# numpy mirrors of the C structs (packed exactly like the C layout)
+PAIR_DTYPE = np.dtype([("a_off", "<u8"), ("b_off", "<u8"), ("a_len", "<u4"), ("b_len", "<u4")])
+RESULT_DTYPE = np.dtype(
+    [
+        ("score", "<i4"),
+        ("i_begin", "<i4"),
+        ("i_end", "<i4"),
+        ("j_begin", "<i4"),
+        ("j_end", "<i4"),
+        ("matches", "<i4"),
+        ("aln_len", "<i4"),
+        ("status", "<i4"),
+    ]
+)
+assert PAIR_DTYPE.itemsize == 24 and RESULT_DTYPE.itemsize == 32
+
+SW_OK, SW_EINVAL, SW_ECUDA, SW_EINTERNAL = 0, -1, -2, -3
+STATUS_OK, STATUS_EMPTY, STATUS_INTERNAL = 0, 1, 2
+
+# every symbol include/pastis_sw.h declares
+EXPORTED_SYMBOLS = (
+    "sw_get_device_count",
+    "sw_last_error",
+    "sw_abi_version",
+    "sw_align_batch",
+    "sw_align_batch_device",
+    "sw_align_batch_multi",
+    "sw_partition_pairs",
+    "sw_release",
+    "sw_host_alloc",
+    "sw_host_free",
+)
+
+
+class SwParams(ctypes.Structure):
+    _fields_ = [("gap_open", ctypes.c_int32), ("gap_extend", ctypes.c_int32),
+                ("matrix", ctypes.c_int32 * 625)]
+
+
+class SwTiming(ctypes.Structure):
+    _fields_ = [
+        ("forward_ms", ctypes.c_double),
+        ("reverse_ms", ctypes.c_double),
+        ("traceback_ms", ctypes.c_double),
+        ("kernel_ms", ctypes.c_double),
+        ("h2d_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("total_ms", ctypes.c_double),
+        ("cells", ctypes.c_uint64),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
+        ("launches", ctypes.c_uint32),
+        ("wide_pairs", ctypes.c_uint32),
+        ("box_cells", ctypes.c_uint64),
+        ("rev_cells", ctypes.c_uint64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: Optional[str] = None) -> ctypes.CDLL:
+    """Load (once) and type the library; raises if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise NativeError(
+                f"{p} not found: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()')"
+            )
+        lib = ctypes.CDLL(p)
+        vp, u64, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
+        lib.sw_get_device_count.restype = i32
+        lib.sw_get_device_count.argtypes = []
+        lib.sw_last_error.restype = ctypes.c_char_p
+        lib.sw_last_error.argtypes = []
+        lib.sw_abi_version.restype = i32
+        lib.sw_align_batch.restype = i32
+        lib.sw_align_batch.argtypes = [i32, vp, u64, vp, u64, ctypes.POINTER(SwParams), vp,
+                                       ctypes.POINTER(SwTiming)]
+        lib.sw_align_batch_device.restype = i32
+        lib.sw_align_batch_device.argtypes = [i32, vp, u64, vp, u64, ctypes.POINTER(SwParams),
+                                              vp, vp, ctypes.POINTER(SwTiming)]
+        lib.sw_align_batch_multi.restype = i32
+        lib.sw_align_batch_multi.argtypes = [i32, vp, vp, u64, vp, u64,
+                                             ctypes.POINTER(SwParams), vp, vp]
+        lib.sw_partition_pairs.restype = i32
+        lib.sw_partition_pairs.argtypes = [vp, u64, i32, vp, vp]
+        lib.sw_release.restype = None
+        lib.sw_release.argtypes = [i32]
+        lib.sw_host_alloc.restype = vp
+        lib.sw_host_alloc.argtypes = [u64]
+        lib.sw_host_free.restype = None
+        lib.sw_host_free.argtypes = [vp]
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def _check(rc: int) -> None:
+    if rc != SW_OK:
+        msg = load().sw_last_error().decode("utf-8", "replace")
+        if rc == SW_EINVAL:
+            raise ValueError(msg)
+        raise NativeError(f"libpastis_sw error {rc}: {msg}")
+
+
+def device_count() -> int:
+    return int(load().sw_get_device_count())
+
+
+def make_params(gap_open: int, gap_extend: int, matrix) -> SwParams:
+    m = np.ascontiguousarray(np.asarray(matrix, dtype=np.int32)).reshape(-1)
+    if m.size != 625:
+        raise ValueError("substitution matrix must be 25x25")
+    p = SwParams()
+    p.gap_open = int(gap_open)
+    p.gap_extend = int(gap_extend)
+    ctypes.memmove(p.matrix, m.ctypes.data, 625 * 4)
+    return p
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+def align_host(arena: np.ndarray, pairs: np.ndarray, params: SwParams, device: int = 0,
+               out: Optional[np.ndarray] = None):
+    """sw_align_batch: host arena + pair table -> (results, timing dict)."""
+    lib = load()
+    arena = np.ascontiguousarray(arena, dtype=np.uint8)
+    pairs = np.ascontiguousarray(pairs, dtype=PAIR_DTYPE)
+    if out is None:
+        out = np.empty(len(pairs), dtype=RESULT_DTYPE)
+    tm = SwTiming()
+    _check(lib.sw_align_batch(device, _ptr(arena), arena.size, _ptr(pairs), len(pairs),
+                              ctypes.byref(params), _ptr(out), ctypes.byref(tm)))
+    return out, tm.as_dict()
+
+
+def align_multi(arena: np.ndarray, pairs: np.ndarray, params: SwParams, devices):
+    """sw_align_batch_multi: cell-balanced shard over `devices`."""
+    lib = load()
+    arena = np.ascontiguousarray(arena, dtype=np.uint8)
+    pairs = np.ascontiguousarray(pairs, dtype=PAIR_DTYPE)
+    devs = np.asarray(list(devices), dtype=np.int32)
+    out = np.empty(len(pairs), dtype=RESULT_DTYPE)
+    tms = (SwTiming * len(devs))()
+    _check(lib.sw_align_batch_multi(len(devs), devs.ctypes.data, _ptr(arena), arena.size,
+                                    _ptr(pairs), len(pairs), ctypes.byref(params), _ptr(out),
+                                    ctypes.cast(tms, ctypes.c_void_p)))
+    return out, [t.as_dict() for t in tms]
+
+
+def align_device(d_arena: int, arena_bytes: int, d_pairs: int, n_pairs: int, params: SwParams,
+                 d_out: int, device: int = 0, stream: int = 0) -> dict:
+    """sw_align_batch_device on raw device pointers (e.g. torch tensors)."""
+    lib = load()
+    tm = SwTiming()
+    _check(lib.sw_align_batch_device(device, d_arena, arena_bytes, d_pairs, n_pairs,
+                                     ctypes.byref(params), d_out, stream or None,
+                                     ctypes.byref(tm)))
+    return tm.as_dict()
+
+
+def partition(pairs: np.ndarray, n_shards: int):
+    """sw_partition_pairs: LPT cell-balanced shard assignment (host only)."""
+    lib = load()
+    pairs = np.ascontiguousarray(pairs, dtype=PAIR_DTYPE)
+    shard = np.empty(len(pairs), dtype=np.int32)
+    load_ = np.empty(n_shards, dtype=np.uint64)
+    _check(lib.sw_partition_pairs(_ptr(pairs), len(pairs), n_shards, _ptr(shard),
+                                  load_.ctypes.data))
+    return shard, load_

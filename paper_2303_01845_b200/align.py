@@ -1,0 +1,281 @@
+"""Drop-in GPU replacement of pastislite.align (the reference's alignment stage).
+
+Same names, signatures, result fields and error behaviour as
+/root/reference/pkg/src/pastislite/align.py:
+  AlignParams       align.py:37-52   (validation identical)
+  AlignmentResult   align.py:55-67   (same 8 fields, 0-based inclusive spans)
+  AlignmentError    align.py:33-34
+  encode            align.py:70-71
+  smith_waterman    align.py:74-76   (raises AlignmentError on empty input)
+  evaluate_pair     align.py:184-208 (identity / coverage filter)
+  BatchCounters     align.py:211-220
+  align_batch       align.py:223-246 (per-pair error isolation, input order)
+  AlignEngine       align.py:299-347 (start/submit/result/close; lanes = GPUs)
+Every alignment runs on the B200 through libpastis_sw.so (forward, reverse
+and traceback kernels); there is no CPU fallback -- a missing library or GPU
+raises.  Results are bit-identical to the reference's (tests/).
+"""
+
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+from time import perf_counter
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native, blosum62
+from .alphabet import INDEX, SIZE
+from .batch import AlignmentError, PackedBatch, pack_pairs
+from .edges import SimilarityEdge
+
+__all__ = [
+    "AlignParams",
+    "AlignmentResult",
+    "AlignmentError",
+    "BatchCounters",
+    "AlignEngine",
+    "align_batch",
+    "align_packed",
+    "encode",
+    "evaluate_pair",
+    "smith_waterman",
+]
+
+# byte -> alphabet index (align.py:27-30); unknown bytes score as 'X'
+_LUT = np.full(256, INDEX["X"], dtype=np.int64)
+for _sym, _code in INDEX.items():
+    _LUT[ord(_sym)] = _code
+
+
+@dataclass(frozen=True)
+class AlignParams:
+    gap_open: int = 11
+    gap_extend: int = 2
+    matrix: np.ndarray = field(default_factory=lambda: blosum62.MATRIX)
+    min_identity: float = 0.30
+    min_coverage: float = 0.70
+
+    def __post_init__(self):
+        if not (self.gap_open >= self.gap_extend >= 0):
+            raise ValueError("need gap_open >= gap_extend >= 0")
+        mat = np.asarray(self.matrix)
+        if mat.shape != (SIZE, SIZE):
+            raise ValueError(f"substitution matrix must be {SIZE}x{SIZE}")
+        if not np.array_equal(mat, mat.T):
+            raise ValueError("substitution matrix must be symmetric")
+
+
+@dataclass(slots=True)
+class AlignmentResult:
+    """Optimal local alignment; spans are 0-based inclusive residue offsets,
+    all -1 for the empty (score 0) alignment."""
+
+    score: int
+    i_begin: int
+    i_end: int
+    j_begin: int
+    j_end: int
+    matches: int
+    aln_len: int
+    cells: int
+
+
+def encode(residues: str) -> np.ndarray:
+    """Residue indices of `residues` (align.py:70-71)."""
+    return _LUT[np.frombuffer(residues.encode("ascii"), dtype=np.uint8)]
+
+
+_params_cache: dict = {}
+
+
+def _native_params(params: AlignParams) -> "_native.SwParams":
+    key = (params.gap_open, params.gap_extend, id(params.matrix))
+    hit = _params_cache.get(key)
+    if hit is not None and hit[0] is params.matrix:
+        return hit[1]
+    p = _native.make_params(params.gap_open, params.gap_extend,
+                            np.asarray(params.matrix, dtype=np.int32))
+    _params_cache[key] = (params.matrix, p)
+    return p
+
+
+def _device_ids(lanes: int) -> list:
+    n = _native.device_count()
+    if n <= 0:
+        raise _native.NativeError("no CUDA device visible: the GPU aligner has no CPU fallback")
+    env = os.environ.get("PASTIS_SW_DEVICES")
+    ids = [int(x) for x in env.split(",")] if env else list(range(n))
+    return ids[: max(1, min(lanes, len(ids)))]
+
+
+def align_packed(batch: PackedBatch, params: AlignParams, devices=(0,)):
+    """Align a packed batch on the GPU(s).  Returns (records, timings):
+    records is a RESULT_DTYPE array in packed order."""
+    p = _native_params(params)
+    devices = list(devices)
+    if len(batch.pairs) == 0:
+        return np.empty(0, dtype=_native.RESULT_DTYPE), []
+    if len(devices) == 1:
+        rec, tm = _native.align_host(batch.arena, batch.pairs, p, device=devices[0])
+        return rec, [tm]
+    return _native.align_multi(batch.arena, batch.pairs, p, devices)
+
+
+def _to_results(batch: PackedBatch, rec: np.ndarray):
+    """Materialise AlignmentResult objects in input order (API edge only)."""
+    results: list = [None] * batch.n_input
+    errors = list(batch.errors)
+    cells = (batch.pairs["a_len"].astype(np.int64) * batch.pairs["b_len"].astype(np.int64)).tolist()
+    rows = rec.tolist()
+    idx = batch.index.tolist()
+    n_ok = 0
+    cell_sum = 0
+    for k, (row, c) in enumerate(zip(rows, cells)):
+        status = row[7]
+        if status == _native.STATUS_OK:
+            results[idx[k]] = AlignmentResult(row[0], row[1], row[2], row[3], row[4], row[5],
+                                              row[6], c)
+            n_ok += 1
+            cell_sum += c
+        elif status == _native.STATUS_EMPTY:
+            errors.append((idx[k], AlignmentError("cannot align an empty sequence")))
+        else:
+            errors.append((idx[k], AssertionError("traceback lost at H state")))
+    errors.sort(key=lambda e: e[0])
+    return results, errors, n_ok, cell_sum
+
+
+def smith_waterman(a: str, b: str, params: AlignParams) -> AlignmentResult:
+    """Single-pair API (align.py:74-76) on the GPU."""
+    if not a or not b:
+        raise AlignmentError("cannot align an empty sequence")
+    batch = pack_pairs([(a, b, None)])
+    if batch.errors:
+        raise batch.errors[0][1]
+    rec, _ = align_packed(batch, params)
+    results, errors, _, _ = _to_results(batch, rec)
+    if errors:
+        raise errors[0][1]
+    return results[0]
+
+
+def evaluate_pair(
+    i: int,
+    j: int,
+    a: str,
+    b: str,
+    result: AlignmentResult,
+    params: AlignParams,
+) -> Optional[SimilarityEdge]:
+    """Identity/coverage filter (align.py:184-208); returns an edge or None."""
+    if i >= j:
+        raise ValueError(f"pair not canonical: ({i}, {j})")
+    if result.aln_len == 0:
+        return None
+    identity = result.matches / result.aln_len
+    cov_a = (result.i_end - result.i_begin + 1) / len(a)
+    cov_b = (result.j_end - result.j_begin + 1) / len(b)
+    if identity >= params.min_identity and min(cov_a, cov_b) >= params.min_coverage:
+        return SimilarityEdge(i, j, result.score, identity, cov_a, cov_b)
+    return None
+
+
+@dataclass
+class BatchCounters:
+    alignments: int = 0
+    cells: int = 0
+    kernel_seconds: float = 0.0
+
+    def merge(self, other: "BatchCounters") -> None:
+        self.alignments += other.alignments
+        self.cells += other.cells
+        self.kernel_seconds += other.kernel_seconds
+
+
+def _align(pairs: Sequence[tuple], params: AlignParams, devices) -> tuple:
+    batch = pack_pairs(pairs)
+    rec, timings = align_packed(batch, params, devices)
+    results, errors, n_ok, cell_sum = _to_results(batch, rec)
+    # kernel_seconds = forward fill time, the quantity align.py:103-122 times
+    fwd = sum(t["forward_ms"] for t in timings) / 1e3
+    counters = BatchCounters(alignments=n_ok, cells=cell_sum, kernel_seconds=fwd)
+    return results, errors, counters, timings
+
+
+def align_batch(pairs: Sequence[tuple], params: AlignParams) -> tuple:
+    """Align (seq_a, seq_b, payload) tuples in order (align.py:223-246).
+
+    Returns (results, errors, counters); a failing pair leaves None in its
+    result slot and an (index, exception) entry instead of aborting."""
+    results, errors, counters, _ = _align(pairs, params, _device_ids(1))
+    return results, errors, counters
+
+
+class _Pending:
+    """Handle for a submitted batch (align.py:272-296)."""
+
+    def __init__(self, future=None, resolved=None):
+        self._future = future
+        self._resolved = resolved
+
+    def result(self) -> tuple:
+        if self._resolved is None:
+            self._resolved = self._future.result()
+        return self._resolved
+
+
+class AlignEngine:
+    """GPU alignment engine with the reference's interface (align.py:299-347).
+
+    `lanes` = number of GPUs a batch is sharded over (cell-balanced, capped at
+    the visible device count).  With use_processes=True, submit() returns
+    immediately and the batch runs on a host thread (the reference's async
+    pool semantics, needed by pre-blocking, pipeline.py:209-212)."""
+
+    def __init__(self, params: AlignParams, lanes: int = 1, use_processes: bool = False):
+        if lanes < 1:
+            raise ValueError("need at least one alignment lane")
+        self.params = params
+        self.lanes = lanes
+        self.use_processes = use_processes
+        self._pool: Optional[ThreadPoolExecutor] = None
+        self._devices: Optional[list] = None
+        self._lock = threading.Lock()
+
+    def start(self) -> None:
+        if self._devices is None:
+            self._devices = _device_ids(self.lanes)
+        if self.use_processes and self._pool is None:
+            self._pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="pastis-gpu")
+
+    def _run(self, pairs: list) -> tuple:
+        t0 = perf_counter()
+        with self._lock:
+            results, errors, counters, timings = _align(pairs, self.params, self._devices)
+        wall = perf_counter() - t0
+        if len(timings) <= 1:
+            lanes = [(self._devices[0], counters.kernel_seconds, wall)]
+        else:
+            lanes = [(dev, t["forward_ms"] / 1e3, t["total_ms"] / 1e3)
+                     for dev, t in zip(self._devices, timings)]
+        return results, errors, counters, lanes
+
+    def submit(self, pairs: list) -> _Pending:
+        self.start()
+        if not self.use_processes:
+            return _Pending(resolved=self._run(pairs))
+        return _Pending(future=self._pool.submit(self._run, pairs))
+
+    def close(self) -> None:
+        if self._pool is not None:
+            self._pool.shutdown(wait=True)
+            self._pool = None
+
+    def __enter__(self):
+        self.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

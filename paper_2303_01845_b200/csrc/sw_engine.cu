@@ -1,0 +1,547 @@
+// sw_engine.cu -- host runtime + C ABI (include/pastis_sw.h) of the B200
+// batched Smith-Waterman aligner.
+//
+// Replaces the reference's batch seam (pastislite.align.align_batch,
+// align.py:223-246, and AlignEngine's process-pool lanes, align.py:299-347)
+// with: raw-byte arena + pair table on the device -> k_encode -> k_classify
+// (length bins) -> K1 forward per bin -> K1 wide re-run of overflowing pairs
+// -> K2 reverse per bin -> K3 box per bin -> k_walk.  One CUDA stream per
+// device; one host thread per device for multi-GPU sharding.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "sw_kernels.cuh"
+
+using namespace pastis;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(SW_ECUDA, std::string(#call " failed: ") + cudaGetErrorString(e_));         \
+  } while (0)
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(want + want / 8, 4096);
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+constexpr int kSmemScore = kMatBytes + kWarpsPerBlock * kProfBytes;
+
+typedef void (*KernelFn)(KArgs, int, int);
+
+struct KernelInfo {
+  KernelFn fn;
+  int grid;
+};
+
+struct DeviceCtx {
+  int device = -1;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DevBuf arena, codes, pairs, out, st, lists, ctrs, stats, mat, lut, bnd, pool;
+  cudaEvent_t ev[16];
+  KernelInfo fwd[kNumClasses], rev[kNumClasses], box[kNumClasses], fwd_wide, rev_wide;
+  int max_warps = 0;
+  bool ready = false;
+};
+
+std::mutex g_ctx_mu;
+std::vector<DeviceCtx *> g_ctx;
+
+template <typename K>
+int setup_kernel(K fn, int sms, KernelInfo &ki, int &max_warps) {
+  CU(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kSmemScore));
+  int nb = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)fn, kWarpsPerBlock * 32,
+                                                   kSmemScore));
+  if (nb < 1) return fail(SW_ECUDA, "kernel cannot be resident (occupancy 0)");
+  ki.fn = (KernelFn)fn;
+  ki.grid = nb * sms;
+  max_warps = std::max(max_warps, ki.grid * kWarpsPerBlock);
+  return SW_OK;
+}
+
+template <int C>
+int setup_classes(DeviceCtx *c) {
+  if constexpr (C < kNumClasses) {
+    constexpr int R = class_rows(C);
+    int rc = setup_kernel(k_score<R, 0, false>, c->sms, c->fwd[C], c->max_warps);
+    if (rc) return rc;
+    rc = setup_kernel(k_score<R, 1, false>, c->sms, c->rev[C], c->max_warps);
+    if (rc) return rc;
+    rc = setup_kernel(k_box<R>, c->sms, c->box[C], c->max_warps);
+    if (rc) return rc;
+    return setup_classes<C + 1>(c);
+  } else {
+    return SW_OK;
+  }
+}
+
+int get_ctx(int device, DeviceCtx **out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0)
+    return fail(SW_ECUDA, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(SW_EINVAL, "device ordinal out of range");
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  if ((int)g_ctx.size() < n) g_ctx.resize(n, nullptr);
+  if (!g_ctx[device]) g_ctx[device] = new DeviceCtx();
+  DeviceCtx *c = g_ctx[device];
+  if (!c->ready) {
+    CU(cudaSetDevice(device));
+    c->device = device;
+    CU(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto &e : c->ev) CU(cudaEventCreate(&e));
+    int rc = setup_classes<0>(c);
+    if (rc) return rc;
+    rc = setup_kernel(k_score<16, 0, true>, c->sms, c->fwd_wide, c->max_warps);
+    if (rc) return rc;
+    rc = setup_kernel(k_score<16, 1, true>, c->sms, c->rev_wide, c->max_warps);
+    if (rc) return rc;
+    // LUT (align.py:27-30) and matrix buffers
+    CU(c->lut.ensure(256));
+    uint8_t lut[256];
+    const char *alpha = "ARNDCQEGHILKMFPSTWYVBZXU*";
+    for (int i = 0; i < 256; ++i) lut[i] = 22;  // 'X'
+    for (int k = 0; k < kAlpha; ++k) lut[(uint8_t)alpha[k]] = (uint8_t)k;
+    CU(cudaMemcpy(c->lut.p, lut, 256, cudaMemcpyHostToDevice));
+    CU(c->mat.ensure(kMatBytes));
+    c->ready = true;
+  }
+  *out = c;
+  return SW_OK;
+}
+
+int check_params(const sw_params_t *p) {
+  if (!p) return fail(SW_EINVAL, "params is NULL");
+  if (!(p->gap_open >= p->gap_extend && p->gap_extend >= 0))
+    return fail(SW_EINVAL, "need gap_open >= gap_extend >= 0");
+  if (p->gap_open > 16383)
+    return fail(SW_EINVAL, "gap_open > 16383 is outside the GPU aligner's supported domain");
+  for (int i = 0; i < 25; ++i)
+    for (int j = 0; j < 25; ++j) {
+      const int32_t v = p->matrix[i * 25 + j];
+      if (v < -127 || v > 127)
+        return fail(SW_EINVAL, "substitution scores must lie in [-127, 127] for the GPU aligner");
+      if (v != p->matrix[j * 25 + i]) return fail(SW_EINVAL, "substitution matrix must be symmetric");
+    }
+  return SW_OK;
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Core device pipeline.  Caller holds c->mu and has set the device.
+int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
+               const sw_pair_t *d_pairs, uint64_t n_pairs, const sw_params_t *prm,
+               sw_result_t *d_out, cudaStream_t s, sw_timing_t *tm) {
+  if (n_pairs == 0) return SW_OK;
+  if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
+  uint32_t launches = 0;
+  // device buffers
+  CU(c->codes.ensure(arena_bytes + 64));
+  CU(c->st.ensure(n_pairs * sizeof(PairState)));
+  CU(c->lists.ensure((size_t)kStages * kNumClasses * n_pairs * 4));
+  CU(c->ctrs.ensure(2 * kStages * kNumClasses * 4));
+  CU(c->stats.ensure(4 * 8));
+  // int8 matrix incl. the virtual code 25 (-128 everywhere)
+  int8_t mat[kMatBytes];
+  memset(mat, 0, sizeof(mat));
+  for (int i = 0; i < kCodes; ++i)
+    for (int j = 0; j < kCodes; ++j)
+      mat[i * kCodes + j] =
+          (i == kPad || j == kPad) ? (int8_t)-128 : (int8_t)prm->matrix[i * 25 + j];
+  CU(cudaMemcpyAsync(c->mat.p, mat, kCodes * kCodes, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(c->ctrs.p, 0, 2 * kStages * kNumClasses * 4, s));
+  CU(cudaMemsetAsync(c->stats.p, 0, 4 * 8, s));
+
+  KArgs A;
+  memset(&A, 0, sizeof(A));
+  A.codes = (const uint8_t *)c->codes.p;
+  A.raw = d_arena;
+  A.pairs = d_pairs;
+  A.st = (PairState *)c->st.p;
+  A.out = d_out;
+  A.mat = (const int8_t *)c->mat.p;
+  A.lists = (uint32_t *)c->lists.p;
+  A.ctrs = (uint32_t *)c->ctrs.p;
+  A.n_pairs = n_pairs;
+  A.open_ = prm->gap_open;
+  A.ext = prm->gap_extend;
+
+  CU(cudaEventRecord(c->ev[0], s));
+  {
+    const int threads = 256;
+    uint64_t blocks = std::min<uint64_t>((arena_bytes / 16 + threads) / threads + 1, (uint64_t)c->sms * 8);
+    k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, (uint8_t *)c->codes.p, arena_bytes,
+                                                 (const uint8_t *)c->lut.p);
+    ++launches;
+    k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(A, (unsigned long long *)c->stats.p);
+    ++launches;
+    CU(cudaGetLastError());
+  }
+  unsigned long long stats[4] = {0, 0, 0, 0};
+  CU(cudaMemcpyAsync(stats, c->stats.p, 3 * 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const uint64_t cells = stats[0];
+  const uint64_t max_b = stats[1];
+  // per-warp boundary rows for multi-strip pairs
+  A.bnd_stride = max_b + 64;
+  CU(c->bnd.ensure((size_t)c->max_warps * A.bnd_stride * sizeof(int2)));
+  A.bnd = (int2 *)c->bnd.p;
+  // traceback code pool (grow-only; overflow falls back to retry rounds)
+  {
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    const size_t want = std::max<size_t>((size_t)(cells * 0.6) + (64ull << 20), 256ull << 20);
+    const size_t cap = std::min<size_t>({want, (size_t)((free_b + c->pool.bytes) * 0.6),
+                                         (size_t)24 << 30});
+    if (c->pool.bytes < cap) {
+      c->pool.release();
+      CU(c->pool.ensure(cap));
+    }
+  }
+  A.pool = (uint8_t *)c->pool.p;
+  A.pool_cap = c->pool.bytes - 64;  // headroom for the widest vector store
+  CU(c->ctrs.ensure(2 * kStages * kNumClasses * 4));
+  // pool_top lives in the stats buffer slot 3
+  A.pool_top = (unsigned long long *)c->stats.p + 3;
+  CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
+
+  CU(cudaEventRecord(c->ev[1], s));
+  for (int cls = 0; cls < kNumClasses; ++cls) {
+    c->fwd[cls].fn<<<c->fwd[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 0, cls);
+    ++launches;
+  }
+  c->fwd_wide.fn<<<c->fwd_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 3, 0);
+  ++launches;
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(c->ev[2], s));
+  for (int cls = 0; cls < kNumClasses; ++cls) {
+    c->rev[cls].fn<<<c->rev[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 1, cls);
+    ++launches;
+  }
+  c->rev_wide.fn<<<c->rev_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 4, 0);
+  ++launches;
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(c->ev[3], s));
+  double tb_ms = 0.0;
+  for (int round = 0;; ++round) {
+    for (int cls = 0; cls < kNumClasses; ++cls) {
+      c->box[cls].fn<<<c->box[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 2, cls);
+      ++launches;
+    }
+    k_walk<<<(unsigned)((n_pairs + 127) / 128), 128, 0, s>>>(A, nullptr, 0);
+    ++launches;
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(c->ev[4], s));
+    uint32_t retry = 0;
+    CU(cudaMemcpyAsync(&retry, (uint32_t *)c->ctrs.p + 5 * kNumClasses, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    tb_ms += ev_ms(round == 0 ? c->ev[3] : c->ev[5], c->ev[4]);
+    if (retry == 0) break;
+    if (round > 64) return fail(SW_EINTERNAL, "traceback code pool too small for one pair");
+    // requeue: reset K3 lists, pool, retry list
+    CU(cudaEventRecord(c->ev[5], s));
+    uint32_t *ctrs = (uint32_t *)c->ctrs.p;
+    CU(cudaMemsetAsync(ctrs + 2 * kNumClasses, 0, kNumClasses * 4, s));
+    CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 2 * kNumClasses, 0, kNumClasses * 4, s));
+    CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
+    k_requeue<<<64, 256, 0, s>>>(A);
+    ++launches;
+    CU(cudaMemsetAsync(ctrs + 5 * kNumClasses, 0, 4, s));
+    CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 5 * kNumClasses, 0, 4, s));
+  }
+  if (tm) {
+    tm->forward_ms += ev_ms(c->ev[1], c->ev[2]);
+    tm->reverse_ms += ev_ms(c->ev[2], c->ev[3]);
+    tm->traceback_ms += tb_ms;
+    tm->kernel_ms += ev_ms(c->ev[0], c->ev[1]) + ev_ms(c->ev[1], c->ev[3]) + tb_ms;
+    tm->cells += cells;
+    tm->launches += launches;
+    uint32_t h_ctrs[kStages * kNumClasses];
+    CU(cudaMemcpy(h_ctrs, c->ctrs.p, sizeof(h_ctrs), cudaMemcpyDeviceToHost));
+    tm->wide_pairs += h_ctrs[3 * kNumClasses];
+  }
+  return SW_OK;
+}
+
+int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
+               uint64_t n_pairs, const sw_params_t *params, sw_result_t *out, sw_timing_t *tm) {
+  const double t0 = now_ms();
+  int rc = check_params(params);
+  if (rc) return rc;
+  if (n_pairs && (!pairs || !out)) return fail(SW_EINVAL, "NULL pairs/out");
+  for (uint64_t k = 0; k < n_pairs; ++k) {
+    const sw_pair_t &p = pairs[k];
+    if (p.a_off + p.a_len > arena_bytes || p.b_off + p.b_len > arena_bytes)
+      return fail(SW_EINVAL, "pair references bytes outside the arena");
+    if (p.a_len > 65000 || p.b_len > 65000)
+      return fail(SW_EINVAL, "sequence longer than 65000 residues");
+  }
+  DeviceCtx *c = nullptr;
+  rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(c->mu);
+  CU(cudaSetDevice(device));
+  if (tm) memset(tm, 0, sizeof(*tm));
+  if (n_pairs == 0) return SW_OK;
+  cudaStream_t s = c->stream;
+  CU(c->arena.ensure(arena_bytes + 64));
+  CU(c->pairs.ensure(n_pairs * sizeof(sw_pair_t)));
+  CU(c->out.ensure(n_pairs * sizeof(sw_result_t)));
+  CU(cudaEventRecord(c->ev[8], s));
+  CU(cudaMemcpyAsync(c->arena.p, arena, arena_bytes, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->pairs.p, pairs, n_pairs * sizeof(sw_pair_t), cudaMemcpyHostToDevice, s));
+  CU(cudaEventRecord(c->ev[9], s));
+  rc = run_device(c, (const uint8_t *)c->arena.p, arena_bytes, (const sw_pair_t *)c->pairs.p,
+                  n_pairs, params, (sw_result_t *)c->out.p, s, tm);
+  if (rc) return rc;
+  CU(cudaEventRecord(c->ev[10], s));
+  CU(cudaMemcpyAsync(out, c->out.p, n_pairs * sizeof(sw_result_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaEventRecord(c->ev[11], s));
+  CU(cudaStreamSynchronize(s));
+  if (tm) {
+    tm->h2d_ms = ev_ms(c->ev[8], c->ev[9]);
+    tm->d2h_ms = ev_ms(c->ev[10], c->ev[11]);
+    tm->h2d_bytes = arena_bytes + n_pairs * sizeof(sw_pair_t);
+    tm->d2h_bytes = n_pairs * sizeof(sw_result_t);
+    tm->total_ms = now_ms() - t0;
+  }
+  return SW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sw_abi_version(void) { return SW_ABI_VERSION; }
+
+int sw_get_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+const char *sw_last_error(void) { return g_err.c_str(); }
+
+int sw_align_batch(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
+                   uint64_t n_pairs, const sw_params_t *params, sw_result_t *out,
+                   sw_timing_t *timing) {
+  return align_host(device, arena, arena_bytes, pairs, n_pairs, params, out, timing);
+}
+
+int sw_align_batch_device(int device, const uint8_t *d_arena, uint64_t arena_bytes,
+                          const sw_pair_t *d_pairs, uint64_t n_pairs, const sw_params_t *params,
+                          sw_result_t *d_out, void *stream, sw_timing_t *timing) {
+  const double t0 = now_ms();
+  int rc = check_params(params);
+  if (rc) return rc;
+  DeviceCtx *c = nullptr;
+  rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(c->mu);
+  CU(cudaSetDevice(device));
+  if (timing) memset(timing, 0, sizeof(*timing));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  rc = run_device(c, d_arena, arena_bytes, d_pairs, n_pairs, params, d_out, s, timing);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(s));
+  if (timing) timing->total_ms = now_ms() - t0;
+  return SW_OK;
+}
+
+int sw_partition_pairs(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards, int32_t *shard,
+                       uint64_t *load) {
+  if (n_shards < 1) return fail(SW_EINVAL, "n_shards < 1");
+  if (n_pairs && (!pairs || !shard)) return fail(SW_EINVAL, "NULL pairs/shard");
+  std::vector<uint64_t> order(n_pairs);
+  std::iota(order.begin(), order.end(), 0ull);
+  auto cells = [&](uint64_t k) { return (uint64_t)pairs[k].a_len * pairs[k].b_len; };
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint64_t x, uint64_t y) { return cells(x) > cells(y); });
+  typedef std::pair<uint64_t, int> Slot;  // (load, shard)
+  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+  std::vector<uint64_t> ld(n_shards, 0);
+  for (int s = 0; s < n_shards; ++s) heap.push(Slot(0, s));
+  for (uint64_t k : order) {
+    Slot t = heap.top();
+    heap.pop();
+    shard[k] = t.second;
+    t.first += cells(k);
+    ld[t.second] = t.first;
+    heap.push(t);
+  }
+  if (load)
+    for (int s = 0; s < n_shards; ++s) load[s] = ld[s];
+  return SW_OK;
+}
+
+int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena,
+                         uint64_t arena_bytes, const sw_pair_t *pairs, uint64_t n_pairs,
+                         const sw_params_t *params, sw_result_t *out,
+                         sw_timing_t *per_device_timing) {
+  if (n_devices < 1 || !devices) return fail(SW_EINVAL, "need at least one device");
+  int rc = check_params(params);
+  if (rc) return rc;
+  if (n_devices == 1)
+    return align_host(devices[0], arena, arena_bytes, pairs, n_pairs, params, out,
+                      per_device_timing);
+  std::vector<int32_t> shard(n_pairs);
+  rc = sw_partition_pairs(pairs, n_pairs, n_devices, shard.data(), nullptr);
+  if (rc) return rc;
+  // per-shard deduplicated arenas + pair tables
+  struct Shard {
+    std::vector<uint8_t> arena;
+    std::vector<sw_pair_t> pairs;
+    std::vector<uint64_t> idx;
+    std::vector<sw_result_t> out;
+    int rc = 0;
+    std::string err;
+  };
+  std::vector<Shard> sh(n_devices);
+  std::vector<std::unordered_map<uint64_t, uint64_t>> seen(n_devices);
+  auto place = [&](Shard &S, std::unordered_map<uint64_t, uint64_t> &m, uint64_t off,
+                   uint32_t len) -> uint64_t {
+    const uint64_t key = off * 131071ull ^ len;
+    auto it = m.find(key);
+    if (it != m.end()) return it->second;
+    const uint64_t at = (S.arena.size() + 15) & ~15ull;
+    S.arena.resize(at + len);
+    if (len) memcpy(S.arena.data() + at, arena + off, len);
+    m.emplace(key, at);
+    return at;
+  };
+  for (uint64_t k = 0; k < n_pairs; ++k) {
+    const sw_pair_t &p = pairs[k];
+    if (p.a_off + p.a_len > arena_bytes || p.b_off + p.b_len > arena_bytes)
+      return fail(SW_EINVAL, "pair references bytes outside the arena");
+    Shard &S = sh[shard[k]];
+    sw_pair_t q = p;
+    q.a_off = place(S, seen[shard[k]], p.a_off, p.a_len);
+    q.b_off = place(S, seen[shard[k]], p.b_off, p.b_len);
+    S.pairs.push_back(q);
+    S.idx.push_back(k);
+  }
+  std::vector<std::thread> th;
+  for (int d = 0; d < n_devices; ++d) {
+    th.emplace_back([&, d]() {
+      Shard &S = sh[d];
+      S.out.resize(S.pairs.size());
+      if (S.arena.empty()) S.arena.resize(16);
+      sw_timing_t *tm = per_device_timing ? per_device_timing + d : nullptr;
+      S.rc = align_host(devices[d], S.arena.data(), S.arena.size(), S.pairs.data(),
+                        S.pairs.size(), params, S.out.data(), tm);
+      if (S.rc) S.err = g_err;
+    });
+  }
+  for (auto &t : th) t.join();
+  for (int d = 0; d < n_devices; ++d)
+    if (sh[d].rc) return fail(sh[d].rc, "device " + std::to_string(devices[d]) + ": " + sh[d].err);
+  for (int d = 0; d < n_devices; ++d)
+    for (size_t q = 0; q < sh[d].idx.size(); ++q) out[sh[d].idx[q]] = sh[d].out[q];
+  return SW_OK;
+}
+
+void sw_release(int device) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  for (size_t d = 0; d < g_ctx.size(); ++d) {
+    if (device >= 0 && (int)d != device) continue;
+    DeviceCtx *c = g_ctx[d];
+    if (!c) continue;
+    std::lock_guard<std::mutex> g2(c->mu);
+    cudaSetDevice((int)d);
+    for (DevBuf *b : {&c->arena, &c->codes, &c->pairs, &c->out, &c->st, &c->lists, &c->ctrs,
+                      &c->stats, &c->bnd, &c->pool})
+      b->release();
+  }
+}
+
+// Debug aid (not part of the public header): copy the per-pair scratch state
+// (PairState, 48 B each) of the last batch run on `device` to host memory.
+int sw_debug_pair_state(int device, void *host_out, uint64_t n_pairs) {
+  DeviceCtx *c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(c->mu);
+  CU(cudaSetDevice(device));
+  if (n_pairs * sizeof(PairState) > c->st.bytes) return fail(SW_EINVAL, "n_pairs too large");
+  CU(cudaMemcpy(host_out, c->st.p, n_pairs * sizeof(PairState), cudaMemcpyDeviceToHost));
+  return SW_OK;
+}
+
+int sw_debug_pool(int device, void *host_out, uint64_t bytes) {
+  DeviceCtx *c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(c->mu);
+  CU(cudaSetDevice(device));
+  if (bytes > c->pool.bytes) return fail(SW_EINVAL, "bytes too large");
+  CU(cudaMemcpy(host_out, c->pool.p, bytes, cudaMemcpyDeviceToHost));
+  return SW_OK;
+}
+
+void *sw_host_alloc(uint64_t bytes) {
+  void *p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    g_err = "cudaHostAlloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void sw_host_free(void *p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,592 @@
+// sw_kernels.cuh -- sm_100a kernels of the batched Smith-Waterman aligner.
+//
+// Exact restatement, on the GPU, of the reference CPU aligner
+// /root/reference/pkg/src/pastislite/align.py:79-181:
+//   K1 k_score<FWD>  forward fill (align.py:103-121) + row-major-first argmax
+//                    (align.py:124: max score, then min i, then min j)
+//   K2 k_score<REV>  the same fill on the reversed prefixes a[0..i_end],
+//                    b[0..j_end]; the cells reaching `best` there are the
+//                    starts of optimal alignments -> min-box (i0, j0)
+//   K3 k_box         fill of the box [i0..i_end]x[j0..j_end] emitting 4-bit
+//                    traceback codes (Hsrc, Fopen, Eopen) per cell
+//   K4 k_walk        the traceback state machine of align.py:133-169 over
+//                    those codes (box lemma: SURVEY.md App. A.6)
+//
+// Layout: one warp per pair.  Lane t owns R consecutive rows of a 32*R-row
+// strip; at wavefront step s it updates column c = s - t, receiving the row
+// above (H-open, F) from lane t-1 by __shfl_up_sync.  Scores come from a
+// per-warp int8 query profile in shared memory, prof[code][lane][16], read
+// with one 128-bit LDS per step (conflict-free: lane stride 16 B).
+//
+// Forward/reverse passes run in a "scaled" int32 domain: every DP value is
+// held as v * 2^16, so a single DPX op  key = max(h + cc, key)  tracks the
+// per-row maximum AND the column where it was first reached (cc = 65535 - c).
+// That keeps the per-cell cost at 4 DPX + 1 VIMNMX3 + 1 PRMT + 2 IADD.
+// Values are exact while best < 2^15 - 128; a pair whose running maximum
+// reaches that limit is re-run in the "wide" variant (unscaled int32 with
+// 64-bit keys).  The box pass is always unscaled int32.
+#pragma once
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+#include "../../include/pastis_sw.h"
+
+namespace pastis {
+
+constexpr int kAlpha = 25;
+constexpr int kPad = 25;                 // code of virtual cells (outside the matrix)
+constexpr int kCodes = 26;
+constexpr int kLaneBytes = 16;           // profile bytes per lane per code (R <= 16)
+constexpr int kProfStride = 32 * kLaneBytes;
+constexpr int kProfBytes = kCodes * kProfStride;  // 13,312 B per warp
+constexpr int kMatBytes = 688;           // 26*26 int8, padded to 16
+constexpr int kWarpsPerBlock = 4;
+constexpr int kNumClasses = 5;
+constexpr int kStages = 6;               // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry
+constexpr int32_t kScaledLimit = 32767 - 128;
+constexpr int32_t kNegInf = -(1 << 30);
+
+__host__ __device__ constexpr int class_rows(int cls) {
+  return cls == 0 ? 4 : cls == 1 ? 8 : cls == 2 ? 10 : cls == 3 ? 12 : 16;
+}
+__host__ __device__ inline int class_of(int m) {
+  return m <= 128 ? 0 : m <= 256 ? 1 : m <= 320 ? 2 : m <= 384 ? 3 : 4;
+}
+__host__ __device__ constexpr int box_lane_bytes(int R) { return R <= 4 ? 2 : R <= 8 ? 4 : 8; }
+
+enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4 };
+
+struct PairState {         // per-pair scratch between the passes (32 B)
+  int32_t best, i_end, j_end, flags;
+  int32_t i0, j0, box_cls, pad;
+  uint64_t code_off;
+  uint64_t pad2;
+};
+
+struct KArgs {
+  const uint8_t *codes;    // residue codes 0..24 of the arena (k_encode)
+  const uint8_t *raw;      // raw arena bytes (for `matches`, align.py:142)
+  const sw_pair_t *pairs;
+  PairState *st;
+  sw_result_t *out;
+  const int8_t *mat;       // 26x26 int8 (row/col 25 = virtual, -128)
+  uint32_t *lists;         // [kStages][kNumClasses][n_pairs]
+  uint32_t *ctrs;          // count[kStages*kNumClasses], cursor[...] after it
+  uint64_t n_pairs;
+  int2 *bnd;               // per-warp strip boundary rows
+  uint64_t bnd_stride;     // int2 per warp
+  uint8_t *pool;           // traceback code pool
+  uint64_t pool_cap;
+  unsigned long long *pool_top;
+  int32_t open_, ext;
+};
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// byte k of w, sign-extended, times 65536 (scaled) or times 1 (plain)
+__device__ __forceinline__ uint32_t sel_scaled(int k) {
+  return 0x44u | ((uint32_t)k << 8) | ((uint32_t)(k | 8) << 12);
+}
+__device__ __forceinline__ uint32_t sel_plain(int k) {
+  const uint32_t s = (uint32_t)(k | 8);
+  return (uint32_t)k | (s << 4) | (s << 8) | (s << 12);
+}
+__device__ __forceinline__ uint32_t word_of(const uint4 &p, int r) {
+  return r < 4 ? p.x : r < 8 ? p.y : r < 12 ? p.z : p.w;
+}
+
+__device__ __forceinline__ uint32_t *list_of(const KArgs &A, int stage, int cls) {
+  return A.lists + ((uint64_t)stage * kNumClasses + cls) * A.n_pairs;
+}
+__device__ __forceinline__ void list_push(const KArgs &A, int stage, int cls, uint32_t k) {
+  uint32_t pos = atomicAdd(&A.ctrs[stage * kNumClasses + cls], 1u);
+  list_of(A, stage, cls)[pos] = k;
+}
+// warp-cooperative work fetch; returns pair index or -1
+__device__ __forceinline__ int64_t next_item(const KArgs &A, int stage, int cls, int lane) {
+  uint32_t pos = 0;
+  if (lane == 0) pos = atomicAdd(&A.ctrs[kStages * kNumClasses + stage * kNumClasses + cls], 1u);
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  const uint32_t cnt = *(volatile uint32_t *)&A.ctrs[stage * kNumClasses + cls];
+  if (pos >= cnt) return -1;
+  return (int64_t)list_of(A, stage, cls)[pos];
+}
+
+// A sequence view: element x is codes[base + step * x].
+struct View {
+  const uint8_t *p;
+  int step;
+  __device__ __forceinline__ int at(int x) const { return p[(int64_t)step * x]; }
+};
+
+// Build this lane's slice of the query profile for rows row0+lane*R .. +R-1.
+template <int R>
+__device__ __forceinline__ void build_profile(uint8_t *prof, const int8_t *mat, const View &rows,
+                                              int m, int row0, int lane) {
+  int arow[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int x = row0 + lane * R + r;
+    arow[r] = x < m ? rows.at(x) : kPad;
+  }
+#pragma unroll 2
+  for (int code = 0; code < kCodes; ++code) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      w[r >> 2] |= (uint32_t)(uint8_t)mat[code * kCodes + arow[r]] << (8 * (r & 3));
+    *reinterpret_cast<uint4 *>(prof + code * kProfStride + lane * kLaneBytes) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Lane 0 of a strip > 0 reads the previous strip's bottom row through a
+// 32-column register chunk (double-buffered, coalesced loads).
+struct BoundaryReader {
+  int2 cur, nxt;
+  __device__ __forceinline__ void init(const int2 *bnd, int n, int lane, int2 dflt) {
+    cur = lane < n ? bnd[lane] : dflt;
+    nxt = 32 + lane < n ? bnd[32 + lane] : dflt;
+  }
+  __device__ __forceinline__ int2 get(const int2 *bnd, int s, int n, int lane, int2 dflt) {
+    if ((s & 31) == 0 && s > 0) {
+      cur = nxt;
+      const int c = s + 32 + lane;
+      nxt = c < n ? bnd[c] : dflt;
+    }
+    int2 v;
+    v.x = __shfl_sync(0xffffffffu, cur.x, s & 31);
+    v.y = __shfl_sync(0xffffffffu, cur.y, s & 31);
+    return v;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K1/K2: score pass.  MODE 0 = forward (argmax row-major-first),
+// MODE 1 = reverse (max x, max y over cells == best).
+// WIDE=false: scaled int32 (v << 16); WIDE=true: plain int32 + 64-bit keys.
+// ---------------------------------------------------------------------------
+struct ScoreOut {
+  uint64_t fwd;     // (best << 32) | (0xFFFF - row) << 16 | (0xFFFF - col)
+  int32_t rev_x, rev_y;
+  int32_t vmax;     // running max seen (overflow guard)
+};
+
+template <int R, int MODE, bool WIDE>
+__device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat, const View rows,
+                                               const View cols, const int m, const int n,
+                                               const int32_t open_, const int32_t ext,
+                                               const int32_t best_known, int2 *bnd,
+                                               const int lane) {
+  constexpr int SH = WIDE ? 0 : 16;
+  const int32_t OPEN = open_ << SH;
+  const int32_t nEXT = -(ext << SH);
+  const int32_t NEG = kNegInf;
+  ScoreOut res{0ull, 0, 0, 0};
+  const int nstrips = (m + 32 * R - 1) / (32 * R);
+  for (int strip = 0; strip < nstrips; ++strip) {
+    const int row0 = strip * 32 * R;
+    __syncwarp();
+    build_profile<R>(prof, mat, rows, m, row0, lane);
+    __syncwarp();
+    int32_t Ho[R], E[R];
+    typename std::conditional<WIDE, long long, int32_t>::type key[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) { Ho[r] = -OPEN; E[r] = NEG; key[r] = 0; }
+    int32_t hoUpPrev = -OPEN;
+    int32_t botHo = -OPEN, botF = NEG;
+    const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
+    BoundaryReader br;
+    const int2 dflt = make_int2(-OPEN, NEG);
+    if (has_above) br.init(bnd, n, lane, dflt);
+    const int steps = n + 31;
+    int code_next = lane == 0 ? cols.at(0) : kPad;
+    for (int s = 0; s < steps; ++s) {
+      const int c = s - lane;
+      const bool valid = (c >= 0) & (c < n);
+      const int code = code_next;
+      {
+        const int cn = c + 1;
+        code_next = (cn >= 0 && cn < n) ? cols.at(cn) : kPad;
+      }
+      const uint4 pw = *reinterpret_cast<const uint4 *>(prof + code * kProfStride + lane * kLaneBytes);
+      int32_t upHo = __shfl_up_sync(0xffffffffu, botHo, 1);
+      int32_t upF = __shfl_up_sync(0xffffffffu, botF, 1);
+      if (has_above) {
+        const int2 b = br.get(bnd, s, n, lane, dflt);
+        if (lane == 0) { upHo = b.x; upF = b.y; }
+      } else if (lane == 0) {
+        upHo = -OPEN; upF = NEG;
+      }
+      int32_t cc = 0;
+      if (valid) cc = MODE == 0 ? 65535 - c : c + 1;
+      int32_t diag = hoUpPrev;
+      hoUpPrev = upHo;
+      int32_t F = upF, hoUp = upHo;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t w = word_of(pw, r);
+        const int32_t sc = (int32_t)prmt(w, 0u, WIDE ? sel_plain(r & 3) : sel_scaled(r & 3));
+        E[r] = __viaddmax_s32(E[r], nEXT, Ho[r]);
+        F = __viaddmax_s32(F, nEXT, hoUp);
+        const int32_t D = diag + sc + OPEN;
+        const int32_t h = __vimax3_s32_relu(D, E[r], F);
+        diag = Ho[r];
+        const int32_t ho = h - OPEN;
+        Ho[r] = ho;
+        hoUp = ho;
+        if constexpr (WIDE) {
+          const long long kk = ((long long)h << 32) | (uint32_t)cc;
+          key[r] = kk > key[r] ? kk : key[r];
+        } else {
+          key[r] = __viaddmax_s32(ho, cc + OPEN, key[r]);
+        }
+      }
+      botHo = hoUp;
+      botF = F;
+      if (has_below && lane == 31 && valid) bnd[c] = make_int2(botHo, botF);
+    }
+    // strip reduction
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int x = row0 + lane * R + r;
+      if (x >= m) continue;
+      int32_t v, lo;
+      if constexpr (WIDE) { v = (int32_t)(key[r] >> 32); lo = (int32_t)(key[r] & 0xFFFF); }
+      else { v = key[r] >> 16; lo = key[r] & 0xFFFF; }
+      res.vmax = v > res.vmax ? v : res.vmax;
+      if (MODE == 0) {
+        const uint64_t comp = ((uint64_t)(uint32_t)v << 32) | ((uint64_t)(0xFFFF - x) << 16) |
+                              (uint64_t)lo;
+        res.fwd = comp > res.fwd ? comp : res.fwd;
+      } else {
+        if (v >= best_known && lo >= 1) {  // v <= best always; avoid == on a max
+          res.rev_x = x + 1 > res.rev_x ? x + 1 : res.rev_x;
+          res.rev_y = lo > res.rev_y ? lo : res.rev_y;
+        }
+      }
+    }
+  }
+  // warp reduction
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t f = __shfl_xor_sync(0xffffffffu, res.fwd, o);
+    res.fwd = f > res.fwd ? f : res.fwd;
+    const int32_t x = __shfl_xor_sync(0xffffffffu, res.rev_x, o);
+    res.rev_x = x > res.rev_x ? x : res.rev_x;
+    const int32_t y = __shfl_xor_sync(0xffffffffu, res.rev_y, o);
+    res.rev_y = y > res.rev_y ? y : res.rev_y;
+    const int32_t v = __shfl_xor_sync(0xffffffffu, res.vmax, o);
+    res.vmax = v > res.vmax ? v : res.vmax;
+  }
+  return res;
+}
+
+__device__ __forceinline__ void load_matrix(int8_t *smat, const int8_t *mat) {
+  for (int i = threadIdx.x; i < kCodes * kCodes; i += blockDim.x) smat[i] = mat[i];
+  __syncthreads();
+}
+
+template <int R, int MODE, bool WIDE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_score(KArgs A, int stage, int cls) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int8_t *smat = reinterpret_cast<int8_t *>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t *prof = smem + kMatBytes + warp * kProfBytes;
+  load_matrix(smat, A.mat);
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
+  int2 *bnd = A.bnd + gwarp * A.bnd_stride;
+  for (;;) {
+    const int64_t k = next_item(A, stage, cls, lane);
+    if (k < 0) break;
+    const sw_pair_t p = A.pairs[k];
+    PairState *st = A.st + k;
+    if (MODE == 0) {
+      const View rows{A.codes + p.a_off, 1}, cols{A.codes + p.b_off, 1};
+      const ScoreOut o = score_pair<R, 0, WIDE>(prof, smat, rows, cols, (int)p.a_len,
+                                                 (int)p.b_len, A.open_, A.ext, 0, bnd, lane);
+      if (lane == 0) {
+        const int32_t best = (int32_t)(o.fwd >> 32);
+        const int32_t i_end = 0xFFFF - (int32_t)((o.fwd >> 16) & 0xFFFF);
+        const int32_t j_end = 65535 - (int32_t)(o.fwd & 0xFFFF);
+        if (!WIDE && o.vmax >= kScaledLimit) {
+          st->flags = kFlagWide;
+          list_push(A, 3, 0, (uint32_t)k);
+        } else {
+          st->best = best;
+          st->i_end = best > 0 ? i_end : -1;
+          st->j_end = best > 0 ? j_end : -1;
+          st->flags = WIDE ? kFlagWide : 0;
+          if (best > 0) {
+            if (WIDE) list_push(A, 4, 0, (uint32_t)k);
+            else list_push(A, 1, class_of(i_end + 1), (uint32_t)k);
+          }
+        }
+      }
+    } else {
+      const int32_t i_end = st->i_end, j_end = st->j_end, best = st->best;
+      const View rows{A.codes + p.a_off + i_end, -1}, cols{A.codes + p.b_off + j_end, -1};
+      const ScoreOut o = score_pair<R, 1, WIDE>(prof, smat, rows, cols, i_end + 1, j_end + 1,
+                                                 A.open_, A.ext, best, bnd, lane);
+      if (lane == 0) {
+        const int32_t i0 = i_end + 1 - o.rev_x, j0 = j_end + 1 - o.rev_y;
+        st->i0 = i0;
+        st->j0 = j0;
+        list_push(A, 2, class_of(i_end - i0 + 1), (uint32_t)k);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: box fill with 4-bit traceback codes, plain int32.
+// nibble = Hsrc | Fopen << 2 | Eopen << 3, Hsrc: 0 stop (h==0), 1 diag,
+// 2 up (h==F), 3 left (align.py:137-149 priority order).
+// Code layout per pair: [strip][step][lane][box_lane_bytes(R)].
+// ---------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_box(KArgs A, int stage, int cls) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int8_t *smat = reinterpret_cast<int8_t *>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t *prof = smem + kMatBytes + warp * kProfBytes;
+  load_matrix(smat, A.mat);
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
+  int2 *bnd = A.bnd + gwarp * A.bnd_stride;
+  constexpr int BPL = box_lane_bytes(R);
+  const int32_t OPEN = A.open_, EXT = A.ext;
+  for (;;) {
+    const int64_t k = next_item(A, stage, cls, lane);
+    if (k < 0) break;
+    const sw_pair_t p = A.pairs[k];
+    PairState *st = A.st + k;
+    const int i0 = st->i0, j0 = st->j0;
+    const int m = st->i_end - i0 + 1, n = st->j_end - j0 + 1;
+    const int nstrips = (m + 32 * R - 1) / (32 * R);
+    const int steps = n + 31;
+    const uint64_t bytes = (uint64_t)nstrips * steps * 32 * BPL;
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(A.pool_top, (unsigned long long)bytes);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off + bytes > A.pool_cap) {
+      if (lane == 0) {
+        st->flags |= kFlagRetry;
+        list_push(A, 5, 0, (uint32_t)k);
+      }
+      continue;
+    }
+    if (lane == 0) { st->code_off = off; st->box_cls = cls; st->flags &= ~kFlagRetry; }
+    uint8_t *codes_out = A.pool + off;
+    const View rows{A.codes + p.a_off + i0, 1}, cols{A.codes + p.b_off + j0, 1};
+    for (int strip = 0; strip < nstrips; ++strip) {
+      const int row0 = strip * 32 * R;
+      __syncwarp();
+      build_profile<R>(prof, smat, rows, m, row0, lane);
+      __syncwarp();
+      int32_t Ho[R], E[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) { Ho[r] = -OPEN; E[r] = kNegInf; }
+      int32_t hoUpPrev = -OPEN, botHo = -OPEN, botF = kNegInf;
+      const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
+      BoundaryReader br;
+      const int2 dflt = make_int2(-OPEN, kNegInf);
+      if (has_above) br.init(bnd, n, lane, dflt);
+      int code_next = lane == 0 ? cols.at(0) : kPad;
+      uint8_t *strip_out = codes_out + (uint64_t)strip * steps * 32 * BPL + lane * BPL;
+      for (int s = 0; s < steps; ++s) {
+        const int c = s - lane;
+        const bool valid = (c >= 0) & (c < n);
+        const int code = code_next;
+        {
+          const int cn = c + 1;
+          code_next = (cn >= 0 && cn < n) ? cols.at(cn) : kPad;
+        }
+        const uint4 pw = *reinterpret_cast<const uint4 *>(prof + code * kProfStride + lane * kLaneBytes);
+        int32_t upHo = __shfl_up_sync(0xffffffffu, botHo, 1);
+        int32_t upF = __shfl_up_sync(0xffffffffu, botF, 1);
+        if (has_above) {
+          const int2 b = br.get(bnd, s, n, lane, dflt);
+          if (lane == 0) { upHo = b.x; upF = b.y; }
+        } else if (lane == 0) {
+          upHo = -OPEN; upF = kNegInf;
+        }
+        int32_t diag = hoUpPrev;
+        hoUpPrev = upHo;
+        int32_t F = upF, hoUp = upHo;
+        uint32_t lo = 0u, hi = 0u;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int32_t sc = (int32_t)prmt(word_of(pw, r), 0u, sel_plain(r & 3));
+          const int32_t ee = E[r] - EXT, hl = Ho[r];
+          const int32_t e = max(ee, hl);
+          const int32_t ff = F - EXT;
+          const int32_t f = max(ff, hoUp);
+          const int32_t D = diag + sc + OPEN;
+          // NB: never test `x == max(...)`: ptxas 12.9 for sm_100a folds such
+          // equalities into the VIMNMX predicate with the wrong polarity
+          // (tools/selftest/max_pred.cu).  Decide from the max's inputs instead.
+          const int32_t t = __vimax_s32_relu(D, e);  // max(D, e, 0)
+          const int32_t h = max(t, f);
+          const bool zero = (D <= 0) & (e <= 0) & (f <= 0);
+          const bool dg = (D >= e) & (D >= f);
+          const bool up = f >= t;
+          const uint32_t src = zero ? 0u : (dg ? 1u : (up ? 2u : 3u));
+          const uint32_t nib = src | (hoUp >= ff ? 4u : 0u) | (hl >= ee ? 8u : 0u);
+          if (r < 8) lo |= nib << (4 * r);
+          else hi |= nib << (4 * (r - 8));
+          E[r] = e;
+          F = f;
+          diag = hl;
+          Ho[r] = h - OPEN;
+          hoUp = Ho[r];
+        }
+        botHo = hoUp;
+        botF = F;
+        if (has_below && lane == 31 && valid) bnd[c] = make_int2(botHo, botF);
+        uint8_t *dst = strip_out + (uint64_t)s * 32 * BPL;
+        if (BPL == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)lo;
+        else if (BPL == 4) *reinterpret_cast<uint32_t *>(dst) = lo;
+        else *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int box_rows_of(int cls) { return class_rows(cls); }
+
+__device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int R, int BPL, int steps, int rho,
+                                            int kap) {
+  const int strip = rho / (32 * R);
+  const int rr = rho - strip * 32 * R;
+  const int t = rr / R, r = rr - t * R;
+  const int s = kap + t;
+  const uint8_t b = codes[((uint64_t)strip * steps + s) * 32 * BPL + t * BPL + (r >> 1)];
+  return (r & 1) ? (uint32_t)(b >> 4) : (uint32_t)(b & 15u);
+}
+
+// K4: traceback walk, one thread per pair (align.py:133-181).
+__global__ void k_walk(KArgs A, const uint32_t *only, uint32_t n_only) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t k;
+  if (only) {
+    if (t >= n_only) return;
+    k = only[t];
+  } else {
+    if (t >= A.n_pairs) return;
+    k = t;
+  }
+  const sw_pair_t p = A.pairs[k];
+  PairState *st = A.st + k;
+  sw_result_t r;
+  r.score = 0; r.i_begin = r.i_end = r.j_begin = r.j_end = -1;
+  r.matches = 0; r.aln_len = 0; r.status = SW_STATUS_OK;
+  if (p.a_len == 0 || p.b_len == 0) {
+    r.status = SW_STATUS_EMPTY;
+    A.out[k] = r;
+    return;
+  }
+  const int32_t flags = st->flags;
+  if (flags & kFlagDone) return;
+  if (flags & kFlagRetry) return;
+  if (st->best == 0) {
+    A.out[k] = r;
+    st->flags = flags | kFlagDone;
+    return;
+  }
+  const int i0 = st->i0, j0 = st->j0;
+  const int m = st->i_end - i0 + 1, n = st->j_end - j0 + 1;
+  const int R = box_rows_of(st->box_cls);
+  const int BPL = box_lane_bytes(R);
+  const int steps = n + 31;
+  const uint8_t *codes = A.pool + st->code_off;
+  const uint8_t *ra = A.raw + p.a_off + i0, *rb = A.raw + p.b_off + j0;
+  int i = m, j = n, state = 0, matches = 0, aln = 0;
+  bool lost = false;
+  for (;;) {
+    if (state == 0) {
+      if (i == 0 || j == 0) break;
+      const uint32_t nib = code_at(codes, R, BPL, steps, i - 1, j - 1);
+      const uint32_t src = nib & 3u;
+      if (src == 0u) break;
+      if (src == 1u) {
+        matches += ra[i - 1] == rb[j - 1];
+        ++aln; --i; --j;
+      } else {
+        state = (int)src - 1;  // 1 F (up), 2 E (left)
+      }
+    } else if (state == 1) {
+      if (i == 0) { lost = true; break; }
+      const uint32_t nib = code_at(codes, R, BPL, steps, i - 1, j - 1);
+      ++aln; --i;
+      if (nib & 4u) state = 0;
+    } else {
+      if (j == 0) { lost = true; break; }
+      const uint32_t nib = code_at(codes, R, BPL, steps, i - 1, j - 1);
+      ++aln; --j;
+      if (nib & 8u) state = 0;
+    }
+  }
+  r.score = st->best;
+  r.i_begin = i0 + i; r.i_end = st->i_end;
+  r.j_begin = j0 + j; r.j_end = st->j_end;
+  r.matches = matches; r.aln_len = aln;
+  r.status = lost ? SW_STATUS_INTERNAL : SW_STATUS_OK;
+  A.out[k] = r;
+  st->flags = flags | kFlagDone;
+}
+
+// Byte -> residue code (align.py:27-30: unknown bytes score as 'X').
+__global__ void k_encode(const uint8_t *__restrict__ raw, uint8_t *__restrict__ codes, uint64_t n,
+                         const uint8_t *__restrict__ lut) {
+  __shared__ uint8_t slut[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) slut[i] = lut[i];
+  __syncthreads();
+  const uint64_t n16 = n / 16;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 v = reinterpret_cast<const uint4 *>(raw)[i];
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t x = w[q];
+      w[q] = (uint32_t)slut[x & 255u] | ((uint32_t)slut[(x >> 8) & 255u] << 8) |
+             ((uint32_t)slut[(x >> 16) & 255u] << 16) | ((uint32_t)slut[x >> 24] << 24);
+    }
+    reinterpret_cast<uint4 *>(codes)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  for (uint64_t i = n16 * 16 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    codes[i] = slut[raw[i]];
+}
+
+// Classify pairs for K1 by row count; count cells; reset per-pair state.
+__global__ void k_classify(KArgs A, unsigned long long *stats) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= A.n_pairs) return;
+  const sw_pair_t p = A.pairs[k];
+  PairState s;
+  s.best = 0; s.i_end = s.j_end = -1; s.flags = 0; s.i0 = s.j0 = 0; s.box_cls = 0; s.pad = 0;
+  s.code_off = 0; s.pad2 = 0;
+  A.st[k] = s;
+  if (p.a_len == 0 || p.b_len == 0) return;
+  list_push(A, 0, class_of((int)p.a_len), (uint32_t)k);
+  atomicAdd(&stats[0], (unsigned long long)p.a_len * p.b_len);
+  atomicMax(&stats[1], (unsigned long long)p.b_len);
+  atomicMax(&stats[2], (unsigned long long)p.a_len);
+}
+
+// Move retry pairs back into the K3 lists.
+__global__ void k_requeue(KArgs A) {
+  const uint32_t n = A.ctrs[5 * kNumClasses];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint32_t k = list_of(A, 5, 0)[t];
+    list_push(A, 2, class_of(A.st[k].i_end - A.st[k].i0 + 1), k);
+  }
+}
+
+}  // namespace pastis

@@ -1,0 +1,198 @@
+"""GPU parity: the B200 kernels vs the reference's golden vectors and the C oracle.
+
+Every comparison is exact (integer fields).  Runs only on a GPU box
+(`pytest -m gpu`); all calls go through libpastis_sw.so's C ABI.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import FIELDS, expect_tuple, load_golden, matrix
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+import paper_2303_01845_b200 as sw  # noqa: E402
+from paper_2303_01845_b200 import _native, workloads  # noqa: E402
+from paper_2303_01845_b200.batch import pack_codes, pack_pairs  # noqa: E402
+
+
+def _params(go, ge, mname="blosum62"):
+    return sw.AlignParams(gap_open=go, gap_extend=ge, matrix=matrix(mname))
+
+
+def _tuple(res):
+    return tuple(getattr(res, f) for f in FIELDS)
+
+
+def _check_cases(cases):
+    groups = {}
+    for k, c in enumerate(cases):
+        groups.setdefault((c["gap_open"], c["gap_extend"], c["matrix"]), []).append(k)
+    bad = []
+    for (go, ge, mname), idx in groups.items():
+        results, errors, counters = sw.align_batch(
+            [(cases[k]["a"], cases[k]["b"], None) for k in idx], _params(go, ge, mname))
+        assert not errors, errors[:3]
+        for k, res in zip(idx, results):
+            c = cases[k]
+            if _tuple(res) != expect_tuple(c) or res.cells != c["expect"]["cells"]:
+                bad.append((c["kind"], go, ge, c["a"][:30], c["b"][:30], _tuple(res),
+                            expect_tuple(c)))
+    assert not bad, f"{len(bad)} mismatches, first: {bad[:3]}"
+
+
+@pytest.mark.parametrize("name", ["kats.json", "random_pairs.json", "config2_sample.json",
+                                  "long_pairs.json"])
+def test_golden_vectors(name):
+    _check_cases(load_golden(name))
+
+
+def test_single_pair_api():
+    for c in load_golden("kats.json"):
+        res = sw.smith_waterman(c["a"], c["b"], _params(c["gap_open"], c["gap_extend"]))
+        assert _tuple(res) == expect_tuple(c)
+    with pytest.raises(sw.AlignmentError):
+        sw.smith_waterman("", "AAA", _params(11, 1))
+
+
+def test_error_isolation_and_order():
+    pairs = [("AAAA", "AAAA", 0), ("", "A", 1), ("MKV", "MKV", 2), ("Aé", "A", 3),
+             ("WW", "", 4), ("P", "A", 5)]
+    results, errors, counters = sw.align_batch(pairs, _params(11, 2))
+    assert [e[0] for e in errors] == [1, 3, 4]
+    assert isinstance(errors[0][1], sw.AlignmentError)
+    assert isinstance(errors[1][1], UnicodeEncodeError)
+    assert results[1] is None and results[3] is None and results[4] is None
+    assert results[0].score == 16 and results[5].score == 0
+    assert counters.alignments == 3 and counters.cells == 16 + 9 + 1
+
+
+def test_config1_digest_through_engine():
+    """Config 1's 628 pipeline pairs through AlignEngine + evaluate_pair reproduce
+    the reference pipeline's canonical output byte for byte."""
+    d = load_golden("config1.json")
+    res = d["residues"]
+    params = sw.AlignParams()
+    with sw.AlignEngine(params, lanes=1, use_processes=True) as eng:
+        pending = eng.submit([(res[i], res[j], None) for i, j in d["pairs"]])
+        results, errors, counters, lanes = pending.result()
+    assert not errors
+    for r, exp in zip(results, d["results"]):
+        assert list(_tuple(r)) + [r.cells] == exp
+    lines = []
+    for (i, j), r in zip(d["pairs"], results):
+        edge = sw.evaluate_pair(i, j, res[i], res[j], r, params)
+        if edge is not None:
+            lines.append(sw.format_edge_line(edge, d["headers"]))
+    canon = sw.canonical_bytes(lines)
+    assert hashlib.sha256(canon).hexdigest() == d["canonical_sha256"]
+    assert lanes and lanes[0][0] == 0
+
+
+def _oracle_compare(sa, sb, go, ge, mname="blosum62", threads=16):
+    arena, table = pack_codes(sa, sb)
+    rec, tm = _native.align_host(arena, table, _native.make_params(go, ge, matrix(mname)))
+    ref = oracle.align_batch_c(arena, table, go, ge, matrix(mname), threads=threads)
+    got = np.stack([rec[f] for f in FIELDS], axis=1)
+    bad = np.flatnonzero((got != ref[:, :7]).any(axis=1))
+    assert (rec["status"] == 0).all()
+    assert len(bad) == 0, (len(bad), [(int(k), got[k].tolist(), ref[k, :7].tolist())
+                                      for k in bad[:3]])
+    return rec, tm
+
+
+@pytest.mark.parametrize("ge", [1, 2])
+def test_config2_vs_oracle(ge):
+    sa, sb = workloads.config2(3000, seed=11 + ge)
+    _oracle_compare(sa, sb, 11, ge)
+
+
+def test_config3_vs_oracle():
+    sa, sb = workloads.config3(1500, seed=5)
+    _oracle_compare(sa, sb, 11, 1)
+
+
+def test_random_lengths_and_gaps_vs_oracle():
+    rng = np.random.default_rng(1)
+    for go, ge in [(11, 1), (10, 10), (5, 0), (0, 0), (3, 1)]:
+        n = 800
+        la = rng.integers(1, 700, size=n)
+        lb = rng.integers(1, 700, size=n)
+        sa, sb = [], []
+        for x, y in zip(la, lb):
+            a = workloads._random_seq(rng, int(x))
+            if rng.random() < 0.5:
+                b = workloads._fit(rng, workloads._homolog(rng, a, 0.2, 0.05), int(y))
+            else:
+                b = workloads._random_seq(rng, int(y))
+            sa.append(a.tobytes())
+            sb.append(b.tobytes())
+        _oracle_compare(sa, sb, go, ge)
+
+
+def test_long_multistrip_vs_oracle():
+    sa, sb = workloads.config5(6, seed=3, lo=2000, hi=5000)
+    rng = np.random.default_rng(4)
+    a = workloads._random_seq(rng, 4200)
+    sa.append(a.tobytes())
+    sb.append(workloads._fit(rng, workloads._homolog(rng, a, 0.2, 0.04), 3900).tobytes())
+    _oracle_compare(sa, sb, 11, 1)
+
+
+def test_wide_path_vs_oracle():
+    rng = np.random.default_rng(9)
+    sa, sb = [], []
+    for n in (2990, 3000, 3100, 3500):
+        a = np.frombuffer(b"W" * n, dtype=np.uint8).copy()
+        a[rng.integers(0, n, 20)] = ord("C")
+        sa.append(a.tobytes())
+        sb.append(a[: n - 7].tobytes())
+    rec, tm = _oracle_compare(sa, sb, 11, 1)
+    assert tm["wide_pairs"] >= 3
+
+
+def test_order_and_sharding_invariance():
+    sa, sb = workloads.config3(2000, seed=21)
+    arena, table = pack_codes(sa, sb)
+    p = _native.make_params(11, 1, matrix("blosum62"))
+    rec, _ = _native.align_host(arena, table, p)
+    perm = np.random.default_rng(0).permutation(len(table))
+    rec_p, _ = _native.align_host(arena, table[perm], p)
+    assert (rec_p == rec[perm]).all()
+    if _native.device_count() >= 2:
+        rec_m, _ = _native.align_multi(arena, table, p, [0, 1])
+        assert (rec_m == rec).all()
+
+
+def test_symmetric_score_property():
+    sa, sb = workloads.config2(2000, seed=77)
+    arena, table = pack_codes(sa, sb)
+    p = _native.make_params(11, 1, matrix("blosum62"))
+    rec, _ = _native.align_host(arena, table, p)
+    swapped = table.copy()
+    swapped["a_off"], swapped["b_off"] = table["b_off"], table["a_off"]
+    swapped["a_len"], swapped["b_len"] = table["b_len"], table["a_len"]
+    rec_s, _ = _native.align_host(arena, swapped, p)
+    assert (rec_s["score"] == rec["score"]).all()
+
+
+def test_full_config2_properties():
+    """Config 2 at full size: size-independent checks + an oracle sample."""
+    sa, sb = workloads.config2(100_000, seed=2303)
+    arena, table = pack_codes(sa, sb)
+    p = _native.make_params(11, 1, matrix("blosum62"))
+    rec, tm = _native.align_host(arena, table, p)
+    assert (rec["status"] == 0).all()
+    pos = rec["score"] > 0
+    assert ((rec["i_begin"] <= rec["i_end"]) | ~pos).all()
+    assert ((rec["matches"] <= rec["aln_len"]) | ~pos).all()
+    span = np.maximum(rec["i_end"] - rec["i_begin"], rec["j_end"] - rec["j_begin"]) + 1
+    assert ((rec["aln_len"] >= span) | ~pos).all()
+    assert tm["cells"] == 100_000 * 300 * 300
+    pick = np.random.default_rng(1).choice(len(table), 400, replace=False)
+    ref = oracle.align_batch_c(arena, table[pick], 11, 1, matrix("blosum62"), threads=16)
+    got = np.stack([rec[f][pick] for f in FIELDS], axis=1)
+    assert (got == ref[:, :7]).all()
