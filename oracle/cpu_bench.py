@@ -1,0 +1,104 @@
+"""TEST/BENCH INFRASTRUCTURE ONLY -- times the CPU restatements of the
+reference aligner on a bounded sample of a workload (bench.py's cpu_baseline
+leg and `bench.py --impl reference`).
+
+The reference's engine runs pairs in forked worker processes, one per lane
+(align.py:299-335); `numpy` mode mirrors that: a fork pool of N processes,
+each running the numpy restatement of align.py:79-181 (oracle.align_numpy).
+`c` mode runs the plain-C restatement threaded over N pthreads.
+Run it in a fresh process (it forks): python -m oracle.cpu_bench --mode numpy
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from oracle import oracle  # noqa: E402
+
+_PAIRS = None
+_GAP = None
+_MAT = None
+
+
+def _init(pairs, gap, mat):
+    global _PAIRS, _GAP, _MAT
+    _PAIRS, _GAP, _MAT = pairs, gap, mat
+
+
+def _run_chunk(bounds):
+    lo, hi = bounds
+    out = []
+    for a, b in _PAIRS[lo:hi]:
+        out.append(oracle.align_numpy(a, b, _GAP[0], _GAP[1], _MAT))
+    return out
+
+
+def sample_pairs(workload: str, n: int, seed: int):
+    from paper_2303_01845_b200 import workloads
+    gen = {"config2": workloads.config2, "config3": workloads.config3,
+           "config5": workloads.config5}[workload]
+    sa, sb = gen(n, seed=seed)
+    return [(a.decode(), b.decode()) for a, b in zip(sa, sb)]
+
+
+def time_numpy(pairs, gap, mat, procs: int) -> dict:
+    import multiprocessing as mp
+    cells = sum(len(a) * len(b) for a, b in pairs)
+    chunk = max(1, len(pairs) // (procs * 8))
+    bounds = [(i, min(len(pairs), i + chunk)) for i in range(0, len(pairs), chunk)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs, initializer=_init, initargs=(pairs, gap, mat)) as pool:
+        pool.map(_run_chunk, bounds[:procs])  # warm the workers
+        t0 = time.perf_counter()
+        res = pool.map(_run_chunk, bounds)
+        dt = time.perf_counter() - t0
+    n = sum(len(r) for r in res)
+    return {"seconds": dt, "pairs": n, "cells": cells, "gcups": cells / dt / 1e9,
+            "aln_per_s": n / dt, "cores": procs}
+
+
+def time_c(pairs, gap, mat, threads: int) -> dict:
+    from paper_2303_01845_b200.batch import pack_codes
+    arena, table = pack_codes([a.encode() for a, _ in pairs], [b.encode() for _, b in pairs])
+    cells = int(np.dot(table["a_len"].astype(np.int64), table["b_len"].astype(np.int64)))
+    oracle.align_batch_c(arena, table[: min(len(table), threads)], gap[0], gap[1], mat, threads)
+    t0 = time.perf_counter()
+    oracle.align_batch_c(arena, table, gap[0], gap[1], mat, threads)
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "pairs": len(table), "cells": cells, "gcups": cells / dt / 1e9,
+            "aln_per_s": len(table) / dt, "cores": threads}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", choices=["numpy", "c"], default="numpy")
+    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--pairs", type=int, default=2000)
+    ap.add_argument("--seed", type=int, default=2303)
+    ap.add_argument("--procs", type=int, default=0)
+    ap.add_argument("--gap-open", type=int, default=11)
+    ap.add_argument("--gap-extend", type=int, default=1)
+    args = ap.parse_args()
+    procs = args.procs or len(os.sched_getaffinity(0))
+    from paper_2303_01845_b200 import blosum62
+    mat = np.asarray(blosum62.MATRIX, dtype=np.int32)
+    pairs = sample_pairs(args.workload, args.pairs, args.seed)
+    gap = (args.gap_open, args.gap_extend)
+    if args.mode == "numpy":
+        r = time_numpy(pairs, gap, mat, procs)
+    else:
+        r = time_c(pairs, gap, mat, procs)
+    r.update({"mode": args.mode, "workload": args.workload})
+    print(json.dumps(r))
+
+
+if __name__ == "__main__":
+    main()
