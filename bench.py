@@ -224,13 +224,18 @@ def main():
                                     n_pairs, params, d_out.data_ptr(), device=local,
                                     stream=stream.cuda_stream)
 
-    for _ in range(args.warmup):
-        device_step()
-    torch.cuda.synchronize()
-    barrier()
     step_ms, fwd_ms, rev_ms, tb_ms, launches = [], [], [], [], 0
     tm = None
     with ClockSampler(local) as clocks:
+        # warm-up also lets the first nvidia-smi query (which stalls the
+        # driver briefly) happen before the timed region
+        for _ in range(args.warmup):
+            device_step()
+        t_wait = time.time()
+        while not clocks.rows and time.time() - t_wait < 10:
+            time.sleep(0.05)
+        torch.cuda.synchronize()
+        barrier()
         for _ in range(args.steps):
             flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)

@@ -322,8 +322,20 @@ k_score(KArgs A, int stage, int cls) {
           st->j_end = best > 0 ? j_end : -1;
           st->flags = WIDE ? kFlagWide : 0;
           if (best > 0) {
-            if (WIDE) list_push(A, 4, 0, (uint32_t)k);
-            else list_push(A, 1, class_of(i_end + 1), (uint32_t)k);
+            // The reverse pass only pays when it can shrink the traceback box
+            // well below the prefix [0..i_end]x[0..j_end].  A homolog's box is
+            // ~(best/3.5)^2 cells; when that is over half the prefix, use the
+            // prefix itself as the box (exact either way: box lemma with
+            // i0 = j0 = 0).  Pure performance choice.
+            const uint64_t area = (uint64_t)(i_end + 1) * (uint64_t)(j_end + 1);
+            const bool skip_rev = WIDE || (uint64_t)best * best * 8ull > 49ull * area;
+            if (skip_rev) {
+              st->i0 = 0;
+              st->j0 = 0;
+              list_push(A, 2, class_of(i_end + 1), (uint32_t)k);
+            } else {
+              list_push(A, 1, class_of(i_end + 1), (uint32_t)k);
+            }
           }
         }
       }
@@ -346,8 +358,82 @@ k_score(KArgs A, int stage, int cls) {
 // K3: box fill with 4-bit traceback codes, plain int32.
 // nibble = Hsrc | Fopen << 2 | Eopen << 3, Hsrc: 0 stop (h==0), 1 diag,
 // 2 up (h==F), 3 left (align.py:137-149 priority order).
-// Code layout per pair: [strip][step][lane][box_lane_bytes(R)].
+// Code layout per pair: [strip][lane][step][box_lane_bytes(R)], steps padded
+// to a multiple of box_steps_per_store(R) so every lane writes whole 16-byte
+// words; a diagonal or horizontal walk step then stays inside the same
+// 32-byte sector for several steps, a vertical one inside the same word.
 // ---------------------------------------------------------------------------
+__host__ __device__ constexpr int box_steps_per_store(int R) { return 16 / box_lane_bytes(R); }
+__host__ __device__ inline int box_padded_steps(int n, int R) {
+  const int f = box_steps_per_store(R);
+  return (n + 31 + f - 1) / f * f;
+}
+
+template <int R>
+struct BoxLane {
+  int32_t Ho[R], E[R];
+  int32_t hoUpPrev, botHo, botF;
+  int code_next;
+};
+
+// One wavefront step of the box fill; returns the lane's R nibbles.
+template <int R>
+__device__ __forceinline__ uint2 box_step(BoxLane<R> &L, const uint8_t *prof, const View &cols,
+                                          int s, int n, int lane, bool has_above, bool has_below,
+                                          BoundaryReader &br, int2 *bnd, const int2 dflt,
+                                          const int32_t OPEN, const int32_t EXT) {
+  const int c = s - lane;
+  const bool valid = (c >= 0) & (c < n);
+  const int code = L.code_next;
+  {
+    const int cn = c + 1;
+    L.code_next = (cn >= 0 && cn < n) ? cols.at(cn) : kPad;
+  }
+  const uint4 pw = *reinterpret_cast<const uint4 *>(prof + code * kProfStride + lane * kLaneBytes);
+  int32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
+  int32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
+  if (has_above) {
+    const int2 b = br.get(bnd, s, n, lane, dflt);
+    if (lane == 0) { upHo = b.x; upF = b.y; }
+  } else if (lane == 0) {
+    upHo = -OPEN; upF = kNegInf;
+  }
+  int32_t diag = L.hoUpPrev;
+  L.hoUpPrev = upHo;
+  int32_t F = upF, hoUp = upHo;
+  uint32_t lo = 0u, hi = 0u;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int32_t sc = (int32_t)prmt(word_of(pw, r), 0u, sel_plain(r & 3));
+    const int32_t ee = L.E[r] - EXT, hl = L.Ho[r];
+    const int32_t e = max(ee, hl);
+    const int32_t ff = F - EXT;
+    const int32_t f = max(ff, hoUp);
+    const int32_t D = diag + sc + OPEN;
+    // NB: never test `x == max(...)`: ptxas 12.9 for sm_100a folds such
+    // equalities into the VIMNMX predicate with the wrong polarity
+    // (tools/selftest/max_pred.cu).  Decide from the max's inputs instead.
+    const int32_t t = __vimax_s32_relu(D, e);  // max(D, e, 0)
+    const int32_t h = max(t, f);
+    const bool zero = (D <= 0) & (e <= 0) & (f <= 0);
+    const bool dg = (D >= e) & (D >= f);
+    const bool up = f >= t;
+    const uint32_t src = zero ? 0u : (dg ? 1u : (up ? 2u : 3u));
+    const uint32_t nib = src | (hoUp >= ff ? 4u : 0u) | (hl >= ee ? 8u : 0u);
+    if (r < 8) lo |= nib << (4 * r);
+    else hi |= nib << (4 * (r - 8));
+    L.E[r] = e;
+    F = f;
+    diag = hl;
+    L.Ho[r] = h - OPEN;
+    hoUp = L.Ho[r];
+  }
+  L.botHo = hoUp;
+  L.botF = F;
+  if (has_below && lane == 31 && valid) bnd[c] = make_int2(L.botHo, L.botF);
+  return make_uint2(lo, hi);
+}
+
 template <int R>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_box(KArgs A, int stage, int cls) {
@@ -359,6 +445,7 @@ k_box(KArgs A, int stage, int cls) {
   const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
   int2 *bnd = A.bnd + gwarp * A.bnd_stride;
   constexpr int BPL = box_lane_bytes(R);
+  constexpr int SPS = box_steps_per_store(R);
   const int32_t OPEN = A.open_, EXT = A.ext;
   for (;;) {
     const int64_t k = next_item(A, stage, cls, lane);
@@ -368,8 +455,8 @@ k_box(KArgs A, int stage, int cls) {
     const int i0 = st->i0, j0 = st->j0;
     const int m = st->i_end - i0 + 1, n = st->j_end - j0 + 1;
     const int nstrips = (m + 32 * R - 1) / (32 * R);
-    const int steps = n + 31;
-    const uint64_t bytes = (uint64_t)nstrips * steps * 32 * BPL;
+    const int spad = box_padded_steps(n, R);
+    const uint64_t bytes = (uint64_t)nstrips * 32 * spad * BPL;
     unsigned long long off = 0;
     if (lane == 0) off = atomicAdd(A.pool_top, (unsigned long long)bytes);
     off = __shfl_sync(0xffffffffu, off, 0);
@@ -381,77 +468,34 @@ k_box(KArgs A, int stage, int cls) {
       continue;
     }
     if (lane == 0) { st->code_off = off; st->box_cls = cls; st->flags &= ~kFlagRetry; }
-    uint8_t *codes_out = A.pool + off;
     const View rows{A.codes + p.a_off + i0, 1}, cols{A.codes + p.b_off + j0, 1};
     for (int strip = 0; strip < nstrips; ++strip) {
       const int row0 = strip * 32 * R;
       __syncwarp();
       build_profile<R>(prof, smat, rows, m, row0, lane);
       __syncwarp();
-      int32_t Ho[R], E[R];
+      BoxLane<R> L;
 #pragma unroll
-      for (int r = 0; r < R; ++r) { Ho[r] = -OPEN; E[r] = kNegInf; }
-      int32_t hoUpPrev = -OPEN, botHo = -OPEN, botF = kNegInf;
+      for (int r = 0; r < R; ++r) { L.Ho[r] = -OPEN; L.E[r] = kNegInf; }
+      L.hoUpPrev = -OPEN; L.botHo = -OPEN; L.botF = kNegInf;
+      L.code_next = lane == 0 ? cols.at(0) : kPad;
       const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
       BoundaryReader br;
       const int2 dflt = make_int2(-OPEN, kNegInf);
       if (has_above) br.init(bnd, n, lane, dflt);
-      int code_next = lane == 0 ? cols.at(0) : kPad;
-      uint8_t *strip_out = codes_out + (uint64_t)strip * steps * 32 * BPL + lane * BPL;
-      for (int s = 0; s < steps; ++s) {
-        const int c = s - lane;
-        const bool valid = (c >= 0) & (c < n);
-        const int code = code_next;
-        {
-          const int cn = c + 1;
-          code_next = (cn >= 0 && cn < n) ? cols.at(cn) : kPad;
-        }
-        const uint4 pw = *reinterpret_cast<const uint4 *>(prof + code * kProfStride + lane * kLaneBytes);
-        int32_t upHo = __shfl_up_sync(0xffffffffu, botHo, 1);
-        int32_t upF = __shfl_up_sync(0xffffffffu, botF, 1);
-        if (has_above) {
-          const int2 b = br.get(bnd, s, n, lane, dflt);
-          if (lane == 0) { upHo = b.x; upF = b.y; }
-        } else if (lane == 0) {
-          upHo = -OPEN; upF = kNegInf;
-        }
-        int32_t diag = hoUpPrev;
-        hoUpPrev = upHo;
-        int32_t F = upF, hoUp = upHo;
-        uint32_t lo = 0u, hi = 0u;
+      uint4 *out = reinterpret_cast<uint4 *>(A.pool + off +
+                                             ((uint64_t)strip * 32 + lane) * spad * BPL);
+      for (int s0 = 0; s0 < spad; s0 += SPS) {
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int32_t sc = (int32_t)prmt(word_of(pw, r), 0u, sel_plain(r & 3));
-          const int32_t ee = E[r] - EXT, hl = Ho[r];
-          const int32_t e = max(ee, hl);
-          const int32_t ff = F - EXT;
-          const int32_t f = max(ff, hoUp);
-          const int32_t D = diag + sc + OPEN;
-          // NB: never test `x == max(...)`: ptxas 12.9 for sm_100a folds such
-          // equalities into the VIMNMX predicate with the wrong polarity
-          // (tools/selftest/max_pred.cu).  Decide from the max's inputs instead.
-          const int32_t t = __vimax_s32_relu(D, e);  // max(D, e, 0)
-          const int32_t h = max(t, f);
-          const bool zero = (D <= 0) & (e <= 0) & (f <= 0);
-          const bool dg = (D >= e) & (D >= f);
-          const bool up = f >= t;
-          const uint32_t src = zero ? 0u : (dg ? 1u : (up ? 2u : 3u));
-          const uint32_t nib = src | (hoUp >= ff ? 4u : 0u) | (hl >= ee ? 8u : 0u);
-          if (r < 8) lo |= nib << (4 * r);
-          else hi |= nib << (4 * (r - 8));
-          E[r] = e;
-          F = f;
-          diag = hl;
-          Ho[r] = h - OPEN;
-          hoUp = Ho[r];
+        for (int q = 0; q < SPS; ++q) {
+          const uint2 v = box_step<R>(L, prof, cols, s0 + q, n, lane, has_above, has_below, br,
+                                      bnd, dflt, OPEN, EXT);
+          if (BPL == 8) { w[2 * q] = v.x; w[2 * q + 1] = v.y; }
+          else if (BPL == 4) { w[q] = v.x; }
+          else { w[q >> 1] |= (v.x & 0xFFFFu) << (16 * (q & 1)); }
         }
-        botHo = hoUp;
-        botF = F;
-        if (has_below && lane == 31 && valid) bnd[c] = make_int2(botHo, botF);
-        uint8_t *dst = strip_out + (uint64_t)s * 32 * BPL;
-        if (BPL == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)lo;
-        else if (BPL == 4) *reinterpret_cast<uint32_t *>(dst) = lo;
-        else *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
+        out[s0 / SPS] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
   }
@@ -459,13 +503,13 @@ k_box(KArgs A, int stage, int cls) {
 
 __device__ __forceinline__ int box_rows_of(int cls) { return class_rows(cls); }
 
-__device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int R, int BPL, int steps, int rho,
+__device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int R, int BPL, int spad, int rho,
                                             int kap) {
   const int strip = rho / (32 * R);
   const int rr = rho - strip * 32 * R;
   const int t = rr / R, r = rr - t * R;
   const int s = kap + t;
-  const uint8_t b = codes[((uint64_t)strip * steps + s) * 32 * BPL + t * BPL + (r >> 1)];
+  const uint8_t b = codes[(((uint64_t)strip * 32 + t) * spad + s) * BPL + (r >> 1)];
   return (r & 1) ? (uint32_t)(b >> 4) : (uint32_t)(b & 15u);
 }
 
@@ -502,7 +546,7 @@ __global__ void k_walk(KArgs A, const uint32_t *only, uint32_t n_only) {
   const int m = st->i_end - i0 + 1, n = st->j_end - j0 + 1;
   const int R = box_rows_of(st->box_cls);
   const int BPL = box_lane_bytes(R);
-  const int steps = n + 31;
+  const int steps = box_padded_steps(n, R);
   const uint8_t *codes = A.pool + st->code_off;
   const uint8_t *ra = A.raw + p.a_off + i0, *rb = A.raw + p.b_off + j0;
   int i = m, j = n, state = 0, matches = 0, aln = 0;
