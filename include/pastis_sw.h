@@ -92,6 +92,8 @@ typedef struct sw_timing_t { /* filled when non-NULL; device times from CUDA eve
   uint32_t wide_pairs;     /* pairs that needed the 32-bit-wide score path */
   uint64_t box_cells;      /* cells recomputed by K3 (sum of box areas) */
   uint64_t rev_cells;      /* cells scored by K2 */
+  double host_plan_ms;     /* host time until the length plan is known (one small sync) */
+  double host_setup_ms;    /* host time spent sizing / allocating cached device buffers */
 } sw_timing_t;
 
 /* Number of visible CUDA devices (0 when none). */

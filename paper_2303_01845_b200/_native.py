@@ -70,6 +70,8 @@ class SwTiming(ctypes.Structure):
         ("wide_pairs", ctypes.c_uint32),
         ("box_cells", ctypes.c_uint64),
         ("rev_cells", ctypes.c_uint64),
+        ("host_plan_ms", ctypes.c_double),
+        ("host_setup_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -60,7 +61,7 @@ struct DevBuf {
   }
 };
 
-constexpr int kSmemScore = kMatBytes + kWarpsPerBlock * kProfBytes;
+constexpr int kSmemScore = kMatBytes + kWarpsPerBlock * (kProfBytes + kStageBytes);
 
 typedef void (*KernelFn)(KArgs, int, int);
 
@@ -76,7 +77,9 @@ struct DeviceCtx {
   std::mutex mu;
   DevBuf arena, codes, pairs, out, st, lists, ctrs, stats, mat, lut, bnd, pool;
   cudaEvent_t ev[16];
-  KernelInfo fwd[kNumClasses], rev[kNumClasses], box[kNumClasses], fwd_wide, rev_wide;
+  KernelInfo fwd[kNumClasses], rev[kNumClasses], box[kNumClasses], ckpt[kNumClasses];
+  KernelInfo tb[kNumClasses];
+  KernelInfo fwd_wide, rev_wide;
   int max_warps = 0;
   bool ready = false;
 };
@@ -98,6 +101,16 @@ int setup_kernel(K fn, int sms, KernelInfo &ki, int &max_warps) {
   return SW_OK;
 }
 
+template <typename K>
+int setup_tb(K fn, int sms, KernelInfo &ki) {
+  int nb = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)fn, kTbWarps * 32, 0));
+  if (nb < 1) return fail(SW_ECUDA, "k_tb cannot be resident");
+  ki.fn = (KernelFn)fn;
+  ki.grid = nb * sms;
+  return SW_OK;
+}
+
 template <int C>
 int setup_classes(DeviceCtx *c) {
   if constexpr (C < kNumClasses) {
@@ -106,7 +119,11 @@ int setup_classes(DeviceCtx *c) {
     if (rc) return rc;
     rc = setup_kernel(k_score<R, 1, false>, c->sms, c->rev[C], c->max_warps);
     if (rc) return rc;
-    rc = setup_kernel(k_box<R>, c->sms, c->box[C], c->max_warps);
+    rc = setup_kernel(k_box<R, false>, c->sms, c->box[C], c->max_warps);
+    if (rc) return rc;
+    rc = setup_kernel(k_score<R, 0, false, true>, c->sms, c->ckpt[C], c->max_warps);
+    if (rc) return rc;
+    rc = setup_tb(k_tb<R>, c->sms, c->tb[C]);
     if (rc) return rc;
     return setup_classes<C + 1>(c);
   } else {
@@ -184,6 +201,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   if (n_pairs == 0) return SW_OK;
   if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
   uint32_t launches = 0;
+  const double h0 = now_ms();
   // device buffers
   CU(c->codes.ensure(arena_bytes + 64));
   CU(c->st.ensure(n_pairs * sizeof(PairState)));
@@ -222,13 +240,22 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, (uint8_t *)c->codes.p, arena_bytes,
                                                  (const uint8_t *)c->lut.p);
     ++launches;
-    k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(A, (unsigned long long *)c->stats.p);
+    // PASTIS_SW_TRACEBACK=box forces the reverse-pass + box traceback for every
+    // pair (A/B comparisons); default: checkpoint + tile replay for pairs
+    // up to kFusedMaxCells cells.
+    static const int allow_ckpt = [] {
+      const char *e = getenv("PASTIS_SW_TRACEBACK");
+      return (e && strcmp(e, "box") == 0) ? 0 : 1;
+    }();
+    k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(A, (unsigned long long *)c->stats.p,
+                                                                allow_ckpt);
     ++launches;
     CU(cudaGetLastError());
   }
   unsigned long long stats[4] = {0, 0, 0, 0};
   CU(cudaMemcpyAsync(stats, c->stats.p, 3 * 8, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  const double h1 = now_ms();
   const uint64_t cells = stats[0];
   const uint64_t max_b = stats[1];
   // per-warp boundary rows for multi-strip pairs
@@ -237,14 +264,17 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   A.bnd = (int2 *)c->bnd.p;
   // traceback code pool (grow-only; overflow falls back to retry rounds)
   {
-    size_t free_b = 0, total_b = 0;
-    CU(cudaMemGetInfo(&free_b, &total_b));
-    const size_t want = std::max<size_t>((size_t)(cells * 0.6) + (64ull << 20), 256ull << 20);
-    const size_t cap = std::min<size_t>({want, (size_t)((free_b + c->pool.bytes) * 0.6),
-                                         (size_t)24 << 30});
-    if (c->pool.bytes < cap) {
-      c->pool.release();
-      CU(c->pool.ensure(cap));
+    // cudaMemGetInfo costs milliseconds: only ask when the pool must grow
+    const size_t want = std::min<size_t>(
+        std::max<size_t>((size_t)(cells * 1.1) + (64ull << 20), 256ull << 20), (size_t)24 << 30);
+    if (c->pool.bytes < want) {
+      size_t free_b = 0, total_b = 0;
+      CU(cudaMemGetInfo(&free_b, &total_b));
+      const size_t cap = std::min<size_t>(want, (size_t)((free_b + c->pool.bytes) * 0.6));
+      if (c->pool.bytes < cap) {
+        c->pool.release();
+        CU(c->pool.ensure(cap));
+      }
     }
   }
   A.pool = (uint8_t *)c->pool.p;
@@ -253,9 +283,14 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   // pool_top lives in the stats buffer slot 3
   A.pool_top = (unsigned long long *)c->stats.p + 3;
   CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
+  const double h2 = now_ms();
 
   CU(cudaEventRecord(c->ev[1], s));
-  for (int cls = 0; cls < kNumClasses; ++cls) {
+  for (int cls = 0; cls < kNumClasses; ++cls) {  // short/medium pairs: forward + checkpoints
+    c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 6, cls);
+    ++launches;
+  }
+  for (int cls = 0; cls < kNumClasses; ++cls) {  // long pairs: score-only forward
     c->fwd[cls].fn<<<c->fwd[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 0, cls);
     ++launches;
   }
@@ -271,6 +306,10 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   ++launches;
   CU(cudaGetLastError());
   CU(cudaEventRecord(c->ev[3], s));
+  for (int cls = 0; cls < kNumClasses; ++cls) {  // tile traceback from the checkpoints
+    c->tb[cls].fn<<<c->tb[cls].grid, kTbWarps * 32, 0, s>>>(A, 7, cls);
+    ++launches;
+  }
   double tb_ms = 0.0;
   for (int round = 0;; ++round) {
     for (int cls = 0; cls < kNumClasses; ++cls) {
@@ -308,6 +347,8 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     uint32_t h_ctrs[kStages * kNumClasses];
     CU(cudaMemcpy(h_ctrs, c->ctrs.p, sizeof(h_ctrs), cudaMemcpyDeviceToHost));
     tm->wide_pairs += h_ctrs[3 * kNumClasses];
+    tm->host_plan_ms += h1 - h0;
+    tm->host_setup_ms += h2 - h1;
   }
   return SW_OK;
 }

@@ -40,9 +40,12 @@ constexpr int kLaneBytes = 16;           // profile bytes per lane per code (R <
 constexpr int kProfStride = 32 * kLaneBytes;
 constexpr int kProfBytes = kCodes * kProfStride;  // 13,312 B per warp
 constexpr int kMatBytes = 688;           // 26*26 int8, padded to 16
+constexpr int kStageBytes = 16 * 8 * 4;  // per-warp row-checkpoint staging (16 boundaries x 8 steps)
 constexpr int kWarpsPerBlock = 4;
 constexpr int kNumClasses = 5;
-constexpr int kStages = 6;               // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry
+constexpr int kStages = 8;  // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
+                            // 6 K1 with checkpoints, 7 tile traceback
+constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take the fused path
 constexpr int32_t kScaledLimit = 32767 - 128;
 constexpr int32_t kNegInf = -(1 << 30);
 
@@ -56,11 +59,11 @@ __host__ __device__ constexpr int box_lane_bytes(int R) { return R <= 4 ? 2 : R 
 
 enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4 };
 
-struct PairState {         // per-pair scratch between the passes (32 B)
+struct PairState {         // per-pair scratch between the passes (48 B)
   int32_t best, i_end, j_end, flags;
-  int32_t i0, j0, box_cls, pad;
-  uint64_t code_off;
-  uint64_t pad2;
+  int32_t i0, j0, box_cls, box_n;  // traceback-code box origin, class (R) and width
+  uint64_t code_off;               // byte offset of the box's codes in the pool
+  int32_t box_m, pad;
 };
 
 struct KArgs {
@@ -169,22 +172,120 @@ struct BoundaryReader {
 // MODE 1 = reverse (max x, max y over cells == best).
 // WIDE=false: scaled int32 (v << 16); WIDE=true: plain int32 + 64-bit keys.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Checkpoints written by the forward pass (short/medium pairs) so that the
+// traceback can replay only the 32-column tiles its path crosses:
+//  * column checkpoints: at the end of every 32-step window w-1 each lane
+//    stores its state entering window w: (Ho_r, E_r) for its R rows plus
+//    (hoUpPrev, F_bot) -> R+1 words of two int16 (unscaled values);
+//  * row checkpoints: "boundary" lanes (the last lane of each group of
+//    G = 32/R lanes, and lane 31) store their bottom-row (Ho, F) every step.
+// Per strip: [window][word (R+1)][lane] words (coalesced stores), then
+// [boundary][step] words.
+// ---------------------------------------------------------------------------
+struct CkLayout {
+  int G, nb, nwin, spad;
+  uint32_t col_words, strip_words;
+};
+__host__ __device__ inline CkLayout ck_layout(int R, int n) {
+  CkLayout L;
+  L.G = 32 / R;
+  L.nb = (32 + L.G - 1) / L.G;
+  L.nwin = (n + 31 + 31) / 32;
+  L.spad = L.nwin * 32;
+  L.col_words = (uint32_t)L.nwin * 32u * (uint32_t)(R + 1);
+  L.strip_words = L.col_words + (uint32_t)L.nb * (uint32_t)L.spad;
+  return L;
+}
+// boundary index of lane t (-1 when t is not a boundary lane)
+__host__ __device__ inline int ck_boundary(int t, const CkLayout &L) {
+  if (t == 31) return L.nb - 1;
+  return ((t + 1) % L.G == 0) ? (t + 1) / L.G - 1 : -1;
+}
+// pack the high halves (the unscaled values) of two scaled words
+__device__ __forceinline__ uint32_t pack_hi16(int32_t lo, int32_t hi) {
+  return prmt((uint32_t)lo, (uint32_t)hi, 0x7632u);
+}
+
 struct ScoreOut {
   uint64_t fwd;     // (best << 32) | (0xFFFF - row) << 16 | (0xFFFF - col)
   int32_t rev_x, rev_y;
   int32_t vmax;     // running max seen (overflow guard)
 };
 
+template <int R, bool WIDE>
+struct ScoreLane {
+  int32_t Ho[R], E[R];
+  typename std::conditional<WIDE, long long, int32_t>::type key[R];
+  int32_t hoUpPrev, botHo, botF;
+  int code_next;
+};
+
+// One wavefront step of the score pass (lane t updates column s - t).
+template <int R, int MODE, bool WIDE>
+__device__ __forceinline__ void score_step(ScoreLane<R, WIDE> &L, const uint8_t *prof,
+                                           const View &cols, const int s, const int n,
+                                           const int lane, const bool has_above,
+                                           const bool has_below, BoundaryReader &br, int2 *bnd,
+                                           const int2 dflt, const int32_t OPEN,
+                                           const int32_t nEXT) {
+  const int c = s - lane;
+  const bool valid = (c >= 0) & (c < n);
+  const int code = L.code_next;
+  {
+    const int cn = c + 1;
+    L.code_next = (cn >= 0 && cn < n) ? cols.at(cn) : kPad;
+  }
+  const uint4 pw = *reinterpret_cast<const uint4 *>(prof + code * kProfStride + lane * kLaneBytes);
+  int32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
+  int32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
+  if (has_above) {
+    const int2 b = br.get(bnd, s, n, lane, dflt);
+    if (lane == 0) { upHo = b.x; upF = b.y; }
+  } else if (lane == 0) {
+    upHo = -OPEN; upF = kNegInf;
+  }
+  int32_t cc = 0;
+  if (valid) cc = MODE == 0 ? 65535 - c : c + 1;
+  int32_t diag = L.hoUpPrev;
+  L.hoUpPrev = upHo;
+  int32_t F = upF, hoUp = upHo;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t w = word_of(pw, r);
+    const int32_t sc = (int32_t)prmt(w, 0u, WIDE ? sel_plain(r & 3) : sel_scaled(r & 3));
+    L.E[r] = __viaddmax_s32(L.E[r], nEXT, L.Ho[r]);
+    F = __viaddmax_s32(F, nEXT, hoUp);
+    const int32_t D = diag + sc + OPEN;
+    const int32_t h = __vimax3_s32_relu(D, L.E[r], F);
+    diag = L.Ho[r];
+    const int32_t ho = h - OPEN;
+    L.Ho[r] = ho;
+    hoUp = ho;
+    if constexpr (WIDE) {
+      const long long kk = ((long long)h << 32) | (uint32_t)cc;
+      L.key[r] = kk > L.key[r] ? kk : L.key[r];
+    } else {
+      L.key[r] = __viaddmax_s32(ho, cc + OPEN, L.key[r]);
+    }
+  }
+  L.botHo = hoUp;
+  L.botF = F;
+  if (has_below && lane == 31 && valid) bnd[c] = make_int2(L.botHo, L.botF);
+}
+
+constexpr int kScoreUnroll = 8;  // steps per unrolled chunk (one 32-B row-checkpoint sector)
+
 template <int R, int MODE, bool WIDE>
 __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat, const View rows,
                                                const View cols, const int m, const int n,
                                                const int32_t open_, const int32_t ext,
                                                const int32_t best_known, int2 *bnd,
-                                               const int lane) {
+                                               const int lane, uint32_t *ck = nullptr,
+                                               uint32_t *ck_stage = nullptr) {
   constexpr int SH = WIDE ? 0 : 16;
   const int32_t OPEN = open_ << SH;
   const int32_t nEXT = -(ext << SH);
-  const int32_t NEG = kNegInf;
   ScoreOut res{0ull, 0, 0, 0};
   const int nstrips = (m + 32 * R - 1) / (32 * R);
   for (int strip = 0; strip < nstrips; ++strip) {
@@ -192,62 +293,62 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
     __syncwarp();
     build_profile<R>(prof, mat, rows, m, row0, lane);
     __syncwarp();
-    int32_t Ho[R], E[R];
-    typename std::conditional<WIDE, long long, int32_t>::type key[R];
+    ScoreLane<R, WIDE> L;
 #pragma unroll
-    for (int r = 0; r < R; ++r) { Ho[r] = -OPEN; E[r] = NEG; key[r] = 0; }
-    int32_t hoUpPrev = -OPEN;
-    int32_t botHo = -OPEN, botF = NEG;
+    for (int r = 0; r < R; ++r) { L.Ho[r] = -OPEN; L.E[r] = kNegInf; L.key[r] = 0; }
+    L.hoUpPrev = -OPEN;
+    L.botHo = -OPEN;
+    L.botF = kNegInf;
+    L.code_next = lane == 0 ? cols.at(0) : kPad;
     const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
     BoundaryReader br;
-    const int2 dflt = make_int2(-OPEN, NEG);
+    const int2 dflt = make_int2(-OPEN, kNegInf);
     if (has_above) br.init(bnd, n, lane, dflt);
     const int steps = n + 31;
-    int code_next = lane == 0 ? cols.at(0) : kPad;
-    for (int s = 0; s < steps; ++s) {
-      const int c = s - lane;
-      const bool valid = (c >= 0) & (c < n);
-      const int code = code_next;
-      {
-        const int cn = c + 1;
-        code_next = (cn >= 0 && cn < n) ? cols.at(cn) : kPad;
-      }
-      const uint4 pw = *reinterpret_cast<const uint4 *>(prof + code * kProfStride + lane * kLaneBytes);
-      int32_t upHo = __shfl_up_sync(0xffffffffu, botHo, 1);
-      int32_t upF = __shfl_up_sync(0xffffffffu, botF, 1);
-      if (has_above) {
-        const int2 b = br.get(bnd, s, n, lane, dflt);
-        if (lane == 0) { upHo = b.x; upF = b.y; }
-      } else if (lane == 0) {
-        upHo = -OPEN; upF = NEG;
-      }
-      int32_t cc = 0;
-      if (valid) cc = MODE == 0 ? 65535 - c : c + 1;
-      int32_t diag = hoUpPrev;
-      hoUpPrev = upHo;
-      int32_t F = upF, hoUp = upHo;
+    // checkpoints (forward pass of short/medium pairs): column checkpoints are
+    // written directly (coalesced, once per 32 steps); row checkpoints are
+    // staged 8 steps at a time in shared memory (stage[b][8]) and flushed as
+    // full 32-byte sectors
+    uint32_t *ck_col = nullptr, *stage_slot = nullptr;
+    uint4 *flush_dst = nullptr;
+    int ck_nwin = 0;
+    if (!WIDE && MODE == 0 && ck) {
+      const CkLayout CL = ck_layout(R, n);
+      uint32_t *base = ck + (uint64_t)strip * CL.strip_words;
+      ck_col = base + lane;
+      const int b = ck_boundary(lane, CL);
+      if (b >= 0) stage_slot = ck_stage + b * kScoreUnroll;
+      if (lane < 2 * CL.nb)
+        flush_dst = reinterpret_cast<uint4 *>(base + CL.col_words + (uint32_t)(lane >> 1) * CL.spad) +
+                    (lane & 1);
+      ck_nwin = CL.nwin;
+    }
+    for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const uint32_t w = word_of(pw, r);
-        const int32_t sc = (int32_t)prmt(w, 0u, WIDE ? sel_plain(r & 3) : sel_scaled(r & 3));
-        E[r] = __viaddmax_s32(E[r], nEXT, Ho[r]);
-        F = __viaddmax_s32(F, nEXT, hoUp);
-        const int32_t D = diag + sc + OPEN;
-        const int32_t h = __vimax3_s32_relu(D, E[r], F);
-        diag = Ho[r];
-        const int32_t ho = h - OPEN;
-        Ho[r] = ho;
-        hoUp = ho;
-        if constexpr (WIDE) {
-          const long long kk = ((long long)h << 32) | (uint32_t)cc;
-          key[r] = kk > key[r] ? kk : key[r];
-        } else {
-          key[r] = __viaddmax_s32(ho, cc + OPEN, key[r]);
+      for (int q = 0; q < kScoreUnroll; ++q) {
+        score_step<R, MODE, WIDE>(L, prof, cols, s0 + q, n, lane, has_above, has_below, br, bnd,
+                                  dflt, OPEN, nEXT);
+        if constexpr (!WIDE && MODE == 0) {
+          if (stage_slot) stage_slot[q] = pack_hi16(L.botHo, L.botF);
         }
       }
-      botHo = hoUp;
-      botF = F;
-      if (has_below && lane == 31 && valid) bnd[c] = make_int2(botHo, botF);
+      if constexpr (!WIDE && MODE == 0) {
+        if (ck_col) {
+          __syncwarp();
+          if (flush_dst) flush_dst[s0 / 4] = reinterpret_cast<const uint4 *>(ck_stage)[lane];
+          __syncwarp();
+        }
+        // window boundary: state after step s0 + 7 == 32w - 1 enters window w
+        if (ck_col && ((s0 + kScoreUnroll) & 31) == 0) {
+          const int w = (s0 + kScoreUnroll) >> 5;
+          if (w < ck_nwin) {
+            uint32_t *dst = ck_col + (uint64_t)w * 32 * (R + 1);
+#pragma unroll
+            for (int r = 0; r < R; ++r) dst[32 * r] = pack_hi16(L.Ho[r], L.E[r]);
+            dst[32 * R] = pack_hi16(L.hoUpPrev, L.botF);
+          }
+        }
+      }
     }
     // strip reduction
 #pragma unroll
@@ -255,8 +356,8 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
       const int x = row0 + lane * R + r;
       if (x >= m) continue;
       int32_t v, lo;
-      if constexpr (WIDE) { v = (int32_t)(key[r] >> 32); lo = (int32_t)(key[r] & 0xFFFF); }
-      else { v = key[r] >> 16; lo = key[r] & 0xFFFF; }
+      if constexpr (WIDE) { v = (int32_t)(L.key[r] >> 32); lo = (int32_t)(L.key[r] & 0xFFFF); }
+      else { v = L.key[r] >> 16; lo = L.key[r] & 0xFFFF; }
       res.vmax = v > res.vmax ? v : res.vmax;
       if (MODE == 0) {
         const uint64_t comp = ((uint64_t)(uint32_t)v << 32) | ((uint64_t)(0xFFFF - x) << 16) |
@@ -290,13 +391,15 @@ __device__ __forceinline__ void load_matrix(int8_t *smat, const int8_t *mat) {
   __syncthreads();
 }
 
-template <int R, int MODE, bool WIDE>
+template <int R, int MODE, bool WIDE, bool CKPT = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_score(KArgs A, int stage, int cls) {
   extern __shared__ __align__(16) uint8_t smem[];
   int8_t *smat = reinterpret_cast<int8_t *>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t *prof = smem + kMatBytes + warp * kProfBytes;
+  uint32_t *ck_stage = reinterpret_cast<uint32_t *>(smem + kMatBytes + kWarpsPerBlock * kProfBytes +
+                                                    warp * kStageBytes);
   load_matrix(smat, A.mat);
   const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
   int2 *bnd = A.bnd + gwarp * A.bnd_stride;
@@ -307,9 +410,30 @@ k_score(KArgs A, int stage, int cls) {
     PairState *st = A.st + k;
     if (MODE == 0) {
       const View rows{A.codes + p.a_off, 1}, cols{A.codes + p.b_off, 1};
+      uint32_t *ck = nullptr;
+      unsigned long long ck_off = 0;
+      if (CKPT) {
+        const CkLayout CL = ck_layout(R, (int)p.b_len);
+        const int nstrips = ((int)p.a_len + 32 * R - 1) / (32 * R);
+        const uint64_t bytes = (uint64_t)nstrips * CL.strip_words * 4ull;
+        if (lane == 0) ck_off = atomicAdd(A.pool_top, (unsigned long long)bytes);
+        ck_off = __shfl_sync(0xffffffffu, ck_off, 0);
+        if (ck_off + bytes <= A.pool_cap) ck = reinterpret_cast<uint32_t *>(A.pool + ck_off);
+      }
       const ScoreOut o = score_pair<R, 0, WIDE>(prof, smat, rows, cols, (int)p.a_len,
-                                                 (int)p.b_len, A.open_, A.ext, 0, bnd, lane);
-      if (lane == 0) {
+                                                 (int)p.b_len, A.open_, A.ext, 0, bnd, lane, ck,
+                                                 ck_stage);
+      if (CKPT && lane == 0 && ck && !(o.vmax >= kScaledLimit) && (o.fwd >> 32) > 0) {
+        st->best = (int32_t)(o.fwd >> 32);
+        st->i_end = 0xFFFF - (int32_t)((o.fwd >> 16) & 0xFFFF);
+        st->j_end = 65535 - (int32_t)(o.fwd & 0xFFFF);
+        st->flags = 0;
+        st->i0 = 0;
+        st->j0 = 0;
+        st->code_off = ck_off;
+        st->box_cls = cls;
+        list_push(A, 7, cls, (uint32_t)k);
+      } else if (lane == 0) {
         const int32_t best = (int32_t)(o.fwd >> 32);
         const int32_t i_end = 0xFFFF - (int32_t)((o.fwd >> 16) & 0xFFFF);
         const int32_t j_end = 65535 - (int32_t)(o.fwd & 0xFFFF);
@@ -369,19 +493,23 @@ __host__ __device__ inline int box_padded_steps(int n, int R) {
   return (n + 31 + f - 1) / f * f;
 }
 
-template <int R>
+template <int R, bool KEY>
 struct BoxLane {
   int32_t Ho[R], E[R];
+  int32_t key[KEY ? R : 1];
   int32_t hoUpPrev, botHo, botF;
   int code_next;
 };
 
 // One wavefront step of the box fill; returns the lane's R nibbles.
-template <int R>
-__device__ __forceinline__ uint2 box_step(BoxLane<R> &L, const uint8_t *prof, const View &cols,
-                                          int s, int n, int lane, bool has_above, bool has_below,
-                                          BoundaryReader &br, int2 *bnd, const int2 dflt,
-                                          const int32_t OPEN, const int32_t EXT) {
+// SCALED: values held as v << 16 (fused pass, with the per-row argmax key);
+// otherwise plain int32.
+template <int R, bool SCALED>
+__device__ __forceinline__ uint2 box_step(BoxLane<R, SCALED> &L, const uint8_t *prof,
+                                          const View &cols, int s, int n, int lane, bool has_above,
+                                          bool has_below, BoundaryReader &br, int2 *bnd,
+                                          const int2 dflt, const int32_t OPEN, const int32_t EXT,
+                                          const bool fwd_key) {
   const int c = s - lane;
   const bool valid = (c >= 0) & (c < n);
   const int code = L.code_next;
@@ -398,13 +526,16 @@ __device__ __forceinline__ uint2 box_step(BoxLane<R> &L, const uint8_t *prof, co
   } else if (lane == 0) {
     upHo = -OPEN; upF = kNegInf;
   }
+  int32_t cc = 0;
+  if (SCALED && valid) cc = fwd_key ? 65535 - c : c + 1;
+  const int32_t ccx = cc + OPEN;
   int32_t diag = L.hoUpPrev;
   L.hoUpPrev = upHo;
   int32_t F = upF, hoUp = upHo;
   uint32_t lo = 0u, hi = 0u;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int32_t sc = (int32_t)prmt(word_of(pw, r), 0u, sel_plain(r & 3));
+    const int32_t sc = (int32_t)prmt(word_of(pw, r), 0u, SCALED ? sel_scaled(r & 3) : sel_plain(r & 3));
     const int32_t ee = L.E[r] - EXT, hl = L.Ho[r];
     const int32_t e = max(ee, hl);
     const int32_t ff = F - EXT;
@@ -425,8 +556,10 @@ __device__ __forceinline__ uint2 box_step(BoxLane<R> &L, const uint8_t *prof, co
     L.E[r] = e;
     F = f;
     diag = hl;
-    L.Ho[r] = h - OPEN;
-    hoUp = L.Ho[r];
+    const int32_t ho = h - OPEN;
+    L.Ho[r] = ho;
+    hoUp = ho;
+    if constexpr (SCALED) L.key[r] = __viaddmax_s32(ho, ccx, L.key[r]);
   }
   L.botHo = hoUp;
   L.botF = F;
@@ -434,7 +567,12 @@ __device__ __forceinline__ uint2 box_step(BoxLane<R> &L, const uint8_t *prof, co
   return make_uint2(lo, hi);
 }
 
-template <int R>
+// K3 (FUSED=false): box [i0..i_end]x[j0..j_end] of a pair whose end cell is
+//   known, plain int32, codes only.
+// K1c (FUSED=true): the whole matrix of a short/medium pair in the scaled
+//   domain: forward score + row-major-first end cell (as k_score<FWD>) AND the
+//   traceback codes in one pass, so such pairs need neither K2 nor K3.
+template <int R, bool FUSED>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_box(KArgs A, int stage, int cls) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -446,37 +584,52 @@ k_box(KArgs A, int stage, int cls) {
   int2 *bnd = A.bnd + gwarp * A.bnd_stride;
   constexpr int BPL = box_lane_bytes(R);
   constexpr int SPS = box_steps_per_store(R);
-  const int32_t OPEN = A.open_, EXT = A.ext;
+  constexpr int SH = FUSED ? 16 : 0;
+  const int32_t OPEN = A.open_ << SH, EXT = A.ext << SH;
   for (;;) {
     const int64_t k = next_item(A, stage, cls, lane);
     if (k < 0) break;
     const sw_pair_t p = A.pairs[k];
     PairState *st = A.st + k;
-    const int i0 = st->i0, j0 = st->j0;
-    const int m = st->i_end - i0 + 1, n = st->j_end - j0 + 1;
+    int i0 = 0, j0 = 0, m, n;
+    if (FUSED) {
+      m = (int)p.a_len;
+      n = (int)p.b_len;
+    } else {
+      i0 = st->i0;
+      j0 = st->j0;
+      m = st->i_end - i0 + 1;
+      n = st->j_end - j0 + 1;
+    }
     const int nstrips = (m + 32 * R - 1) / (32 * R);
     const int spad = box_padded_steps(n, R);
     const uint64_t bytes = (uint64_t)nstrips * 32 * spad * BPL;
     unsigned long long off = 0;
     if (lane == 0) off = atomicAdd(A.pool_top, (unsigned long long)bytes);
     off = __shfl_sync(0xffffffffu, off, 0);
-    if (off + bytes > A.pool_cap) {
+    const bool fits = off + bytes <= A.pool_cap;
+    if (!fits && !FUSED) {
       if (lane == 0) {
         st->flags |= kFlagRetry;
         list_push(A, 5, 0, (uint32_t)k);
       }
       continue;
     }
-    if (lane == 0) { st->code_off = off; st->box_cls = cls; st->flags &= ~kFlagRetry; }
     const View rows{A.codes + p.a_off + i0, 1}, cols{A.codes + p.b_off + j0, 1};
+    uint64_t fwd = 0ull;
+    int32_t vmax = 0;
     for (int strip = 0; strip < nstrips; ++strip) {
       const int row0 = strip * 32 * R;
       __syncwarp();
       build_profile<R>(prof, smat, rows, m, row0, lane);
       __syncwarp();
-      BoxLane<R> L;
+      BoxLane<R, FUSED> L;
 #pragma unroll
       for (int r = 0; r < R; ++r) { L.Ho[r] = -OPEN; L.E[r] = kNegInf; }
+      if constexpr (FUSED) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) L.key[r] = 0;
+      }
       L.hoUpPrev = -OPEN; L.botHo = -OPEN; L.botF = kNegInf;
       L.code_next = lane == 0 ? cols.at(0) : kPad;
       const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
@@ -489,13 +642,69 @@ k_box(KArgs A, int stage, int cls) {
         uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int q = 0; q < SPS; ++q) {
-          const uint2 v = box_step<R>(L, prof, cols, s0 + q, n, lane, has_above, has_below, br,
-                                      bnd, dflt, OPEN, EXT);
+          const uint2 v = box_step<R, FUSED>(L, prof, cols, s0 + q, n, lane, has_above, has_below,
+                                             br, bnd, dflt, OPEN, EXT, true);
           if (BPL == 8) { w[2 * q] = v.x; w[2 * q + 1] = v.y; }
           else if (BPL == 4) { w[q] = v.x; }
           else { w[q >> 1] |= (v.x & 0xFFFFu) << (16 * (q & 1)); }
         }
-        out[s0 / SPS] = make_uint4(w[0], w[1], w[2], w[3]);
+        if (fits) out[s0 / SPS] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      if constexpr (FUSED) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int x = row0 + lane * R + r;
+          if (x >= m) continue;
+          const int32_t v = L.key[r] >> 16, lo = L.key[r] & 0xFFFF;
+          vmax = v > vmax ? v : vmax;
+          const uint64_t comp = ((uint64_t)(uint32_t)v << 32) |
+                                ((uint64_t)(0xFFFF - x) << 16) | (uint64_t)lo;
+          fwd = comp > fwd ? comp : fwd;
+        }
+      }
+    }
+    if constexpr (FUSED) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t f2 = __shfl_xor_sync(0xffffffffu, fwd, o);
+        fwd = f2 > fwd ? f2 : fwd;
+        const int32_t v2 = __shfl_xor_sync(0xffffffffu, vmax, o);
+        vmax = v2 > vmax ? v2 : vmax;
+      }
+    }
+    if (lane == 0) {
+      if (FUSED) {
+        const int32_t best = (int32_t)(fwd >> 32);
+        const int32_t i_end = 0xFFFF - (int32_t)((fwd >> 16) & 0xFFFF);
+        const int32_t j_end = 65535 - (int32_t)(fwd & 0xFFFF);
+        st->i0 = 0;
+        st->j0 = 0;
+        if (vmax >= kScaledLimit) {           // re-run in the wide score path
+          st->flags = kFlagWide;
+          list_push(A, 3, 0, (uint32_t)k);
+        } else {
+          st->best = best;
+          st->i_end = best > 0 ? i_end : -1;
+          st->j_end = best > 0 ? j_end : -1;
+          if (fits) {
+            st->flags = 0;
+            st->code_off = off;
+            st->box_cls = cls;
+            st->box_m = m;
+            st->box_n = n;
+          } else if (best > 0) {              // no room for codes: prefix box via K3
+            st->flags = kFlagRetry;
+            list_push(A, 5, 0, (uint32_t)k);
+          } else {
+            st->flags = 0;
+          }
+        }
+      } else {
+        st->code_off = off;
+        st->box_cls = cls;
+        st->box_m = m;
+        st->box_n = n;
+        st->flags &= ~kFlagRetry;
       }
     }
   }
@@ -511,6 +720,202 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int R, int BPL
   const int s = kap + t;
   const uint8_t b = codes[(((uint64_t)strip * 32 + t) * spad + s) * BPL + (r >> 1)];
   return (r & 1) ? (uint32_t)(b >> 4) : (uint32_t)(b & 15u);
+}
+
+// ---------------------------------------------------------------------------
+// K5: tile traceback for pairs whose forward pass wrote checkpoints.
+// One warp per pair walks the state machine of align.py:133-169 backwards
+// from the end cell.  The 4-bit codes it needs are produced on demand for
+// one tile at a time -- the rows of one lane group (G = 32/R forward lanes,
+// <= 32 rows, one row per replay lane) over one 32-step forward window -- by
+// replaying the forward recurrence from the checkpoints, so only the tiles on
+// the path are recomputed.  The walk is warp-uniform (every lane walks the
+// same path from shared memory).
+// ---------------------------------------------------------------------------
+constexpr int kTbWarps = 4;
+constexpr int kTbCols = 40;   // 32 + G - 1 <= 39 tile columns
+
+struct TbSmem {
+  uint8_t code[32][32];
+  uint8_t bcode[kTbCols], braw[kTbCols];
+  uint8_t araw[32];
+};
+
+__device__ __forceinline__ int32_t lo16(uint32_t x) { return (int32_t)(int16_t)(x & 0xFFFFu); }
+__device__ __forceinline__ int32_t hi16(uint32_t x) { return (int32_t)(int16_t)(x >> 16); }
+
+template <int R>
+__device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const uint32_t *ck,
+                                          const CkLayout &CL, int strip, int g, int w, int m,
+                                          int n, const uint8_t *acodes, const uint8_t *bcodes,
+                                          const uint8_t *araw, const uint8_t *braw, int lane,
+                                          int32_t OPEN, int32_t EXT, int &trow0, int &tcmin,
+                                          const int rho_in, const int kap_in) {
+  const int t0 = g * CL.G;
+  const int t1 = min(t0 + CL.G, 32) - 1;
+  trow0 = strip * 32 * R + t0 * R;
+  const int cmin = 32 * w - t1;
+  const int width = 32 + (t1 - t0);
+  tcmin = cmin;
+  __syncwarp();
+  for (int x = lane; x < width; x += 32) {
+    const int c = cmin + x;
+    const bool ok = (c >= 0) & (c < n);
+    T.bcode[x] = ok ? bcodes[c] : (uint8_t)kPad;
+    T.braw[x] = ok ? braw[c] : (uint8_t)0;
+  }
+  // the walk enters this tile at (rho_in, kap_in) and only moves up/left:
+  // rows below it and columns right of it are never read
+  const int qmax = rho_in - trow0;
+  const int q = lane;
+  const bool row_ok = q <= qmax;
+  const int tq = t0 + q / R, rq = q - (q / R) * R;
+  const int rho = trow0 + q;
+  const bool real_row = row_ok & (rho < m);
+  const int acode = real_row ? acodes[rho] : kPad;
+  if (row_ok) T.araw[q] = real_row ? araw[rho] : (uint8_t)0;
+  const uint32_t *sbase = ck + (uint64_t)strip * CL.strip_words;
+  int32_t Ho = -OPEN, E = kNegInf, hoUpPrevT = -OPEN, FbotT = kNegInf;
+  if (w > 0 && row_ok) {
+    const uint32_t *wd = sbase + (uint64_t)w * 32 * (R + 1) + tq;
+    const uint32_t x = wd[32 * rq], y = wd[32 * R];
+    Ho = lo16(x);
+    E = hi16(x);
+    hoUpPrevT = lo16(y);
+    FbotT = hi16(y);
+  }
+  int32_t outHo = Ho, outF = (rq == R - 1) ? FbotT : kNegInf;
+  const int32_t hoAbove = __shfl_up_sync(0xffffffffu, Ho, 1);
+  int32_t prevTop = (rq == 0) ? hoUpPrevT : hoAbove;
+  // top input of tile row 0 for its 32 columns, one per lane, packed (Ho, F)
+  uint32_t topv = 0xC0000000u | ((uint32_t)(-OPEN) & 0xFFFFu);  // (F = -16384, Ho = -open)
+  {
+    const uint32_t *toprow = nullptr;
+    int tsrc = 0;
+    if (t0 > 0) {
+      toprow = sbase + CL.col_words + (uint64_t)ck_boundary(t0 - 1, CL) * CL.spad;
+      tsrc = t0 - 1;
+    } else if (strip > 0) {
+      toprow = sbase - CL.strip_words + CL.col_words + (uint64_t)(CL.nb - 1) * CL.spad;
+      tsrc = 31;
+    }
+    if (toprow) {
+      const int idx = 32 * w - t0 + lane + tsrc;
+      if (idx >= 0) topv = toprow[idx];
+    }
+  }
+  const int vstart = q - q / R;
+  const int vlast = min(qmax - qmax / R + 31, kap_in - (32 * w - t0) + qmax);
+  for (int v = 0; v <= vlast; ++v) {
+    int32_t topHo = __shfl_up_sync(0xffffffffu, outHo, 1);
+    int32_t topF = __shfl_up_sync(0xffffffffu, outF, 1);
+    const uint32_t tv = __shfl_sync(0xffffffffu, topv, v & 31);
+    if (q == 0) {
+      topHo = lo16(tv);
+      topF = hi16(tv);
+      if (topF == -16384) topF = kNegInf;  // unpacked boundary sentinel
+    }
+    const bool active = row_ok & (v >= vstart) & (v <= vstart + 31);
+    if (active) {
+      const int c = 32 * w - t0 + v - q;
+      const int32_t sc = smat[acode * kCodes + T.bcode[c - cmin]];
+      const int32_t ee = E - EXT, hl = Ho;
+      const int32_t e = max(ee, hl);
+      const int32_t ff = topF - EXT;
+      const int32_t f = max(ff, topHo);
+      const int32_t D = prevTop + sc + OPEN;
+      const int32_t t = __vimax_s32_relu(D, e);
+      const int32_t h = max(t, f);
+      // see box_step: decide from the max's inputs, never `x == max(..)`
+      const bool zero = (D <= 0) & (e <= 0) & (f <= 0);
+      const bool dg = (D >= e) & (D >= f);
+      const bool up = f >= t;
+      const uint32_t src = zero ? 0u : (dg ? 1u : (up ? 2u : 3u));
+      T.code[q][v - vstart] = (uint8_t)(src | (topHo >= ff ? 4u : 0u) | (hl >= ee ? 8u : 0u));
+      E = e;
+      Ho = h - OPEN;
+      outHo = Ho;
+      outF = f;
+      prevTop = topHo;
+    }
+  }
+  __syncwarp();
+}
+
+template <int R>
+__global__ void __launch_bounds__(kTbWarps * 32)
+k_tb(KArgs A, int stage, int cls) {
+  __shared__ int8_t smat[kCodes * kCodes];
+  __shared__ TbSmem tsm[kTbWarps];
+  for (int i = threadIdx.x; i < kCodes * kCodes; i += blockDim.x) smat[i] = A.mat[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TbSmem &T = tsm[warp];
+  const int32_t OPEN = A.open_, EXT = A.ext;
+  for (;;) {
+    const int64_t k = next_item(A, stage, cls, lane);
+    if (k < 0) break;
+    const sw_pair_t p = A.pairs[k];
+    PairState *st = A.st + k;
+    const int m = (int)p.a_len, n = (int)p.b_len;
+    const CkLayout CL = ck_layout(R, n);
+    const uint32_t *ck = reinterpret_cast<const uint32_t *>(A.pool + st->code_off);
+    const uint8_t *acodes = A.codes + p.a_off, *bcodes = A.codes + p.b_off;
+    const uint8_t *araw = A.raw + p.a_off, *braw = A.raw + p.b_off;
+    const int i_end = st->i_end, j_end = st->j_end;
+    int i = i_end + 1, j = j_end + 1, state = 0, matches = 0, aln = 0;
+    int cs = -1, cg = -1, cw = -1, trow0 = 0, tcmin = 0, tqmax = -1;
+    bool lost = false;
+    for (;;) {
+      if (i == 0 || j == 0) {
+        lost = state != 0;
+        break;
+      }
+      const int rho = i - 1, kap = j - 1;
+      // fast path: still inside the replayed part of the current tile
+      int q = rho - trow0;
+      int u = kap - (cw * 32 - (cg * CL.G + q / R));
+      if (!(cs >= 0 && q >= 0 && q <= tqmax && u >= 0 && u < 32)) {
+        const int strip = rho / (32 * R);
+        const int t = (rho - strip * 32 * R) / R;
+        const int g = t / CL.G;
+        const int w = (kap + t) >> 5;
+        tb_replay<R>(T, smat, ck, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+                     EXT, trow0, tcmin, rho, kap);
+        cs = strip; cg = g; cw = w;
+        q = rho - trow0;
+        tqmax = q;
+        u = kap - (32 * w - t);
+      }
+      const uint32_t nib = T.code[q][u];
+      if (state == 0) {
+        const uint32_t src = nib & 3u;
+        if (src == 0u) break;
+        if (src == 1u) {
+          matches += T.araw[q] == T.braw[kap - tcmin];
+          ++aln; --i; --j;
+        } else {
+          state = (int)src - 1;
+        }
+      } else if (state == 1) {
+        ++aln; --i;
+        if (nib & 4u) state = 0;
+      } else {
+        ++aln; --j;
+        if (nib & 8u) state = 0;
+      }
+    }
+    if (lane == 0) {
+      sw_result_t r;
+      r.score = st->best;
+      r.i_begin = i; r.i_end = i_end;
+      r.j_begin = j; r.j_end = j_end;
+      r.matches = matches; r.aln_len = aln;
+      r.status = lost ? SW_STATUS_INTERNAL : SW_STATUS_OK;
+      A.out[k] = r;
+      st->flags |= kFlagDone;
+    }
+  }
 }
 
 // K4: traceback walk, one thread per pair (align.py:133-181).
@@ -543,13 +948,13 @@ __global__ void k_walk(KArgs A, const uint32_t *only, uint32_t n_only) {
     return;
   }
   const int i0 = st->i0, j0 = st->j0;
-  const int m = st->i_end - i0 + 1, n = st->j_end - j0 + 1;
+  const int n = st->box_n;
   const int R = box_rows_of(st->box_cls);
   const int BPL = box_lane_bytes(R);
   const int steps = box_padded_steps(n, R);
   const uint8_t *codes = A.pool + st->code_off;
   const uint8_t *ra = A.raw + p.a_off + i0, *rb = A.raw + p.b_off + j0;
-  int i = m, j = n, state = 0, matches = 0, aln = 0;
+  int i = st->i_end - i0 + 1, j = st->j_end - j0 + 1, state = 0, matches = 0, aln = 0;
   bool lost = false;
   for (;;) {
     if (state == 0) {
@@ -609,16 +1014,17 @@ __global__ void k_encode(const uint8_t *__restrict__ raw, uint8_t *__restrict__ 
 }
 
 // Classify pairs for K1 by row count; count cells; reset per-pair state.
-__global__ void k_classify(KArgs A, unsigned long long *stats) {
+__global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= A.n_pairs) return;
   const sw_pair_t p = A.pairs[k];
   PairState s;
-  s.best = 0; s.i_end = s.j_end = -1; s.flags = 0; s.i0 = s.j0 = 0; s.box_cls = 0; s.pad = 0;
-  s.code_off = 0; s.pad2 = 0;
+  s.best = 0; s.i_end = s.j_end = -1; s.flags = 0; s.i0 = s.j0 = 0; s.box_cls = 0;
+  s.box_n = 0; s.code_off = 0; s.box_m = 0; s.pad = 0;
   A.st[k] = s;
   if (p.a_len == 0 || p.b_len == 0) return;
-  list_push(A, 0, class_of((int)p.a_len), (uint32_t)k);
+  const bool fused = allow_ckpt && (uint64_t)p.a_len * p.b_len <= kFusedMaxCells;
+  list_push(A, fused ? 6 : 0, class_of((int)p.a_len), (uint32_t)k);
   atomicAdd(&stats[0], (unsigned long long)p.a_len * p.b_len);
   atomicMax(&stats[1], (unsigned long long)p.b_len);
   atomicMax(&stats[2], (unsigned long long)p.a_len);
