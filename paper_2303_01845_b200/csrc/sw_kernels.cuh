@@ -725,20 +725,23 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int R, int BPL
 // ---------------------------------------------------------------------------
 // K5: tile traceback for pairs whose forward pass wrote checkpoints.
 // One warp per pair walks the state machine of align.py:133-169 backwards
-// from the end cell.  The 4-bit codes it needs are produced on demand for
-// one tile at a time -- the rows of one lane group (G = 32/R forward lanes,
-// <= 32 rows, one row per replay lane) over one 32-step forward window -- by
-// replaying the forward recurrence from the checkpoints, so only the tiles on
-// the path are recomputed.  The walk is warp-uniform (every lane walks the
-// same path from shared memory).
+// from the end cell.  The H/E/F values it needs are produced on demand for one
+// tile at a time -- the rows of one lane group (G = 32/R forward lanes, <= 32
+// rows, one row per replay lane) over one 32-step forward window -- by
+// replaying the forward recurrence from the checkpoints into a shared-memory
+// tile with a one-cell halo (row above, column left).  Only the tiles on the
+// path are replayed, and only their part the walk can still reach (rows up to
+// and columns up to the entry cell; the walk only moves up/left).  The walk is
+// warp-uniform and compares loaded values exactly as the reference does.
 // ---------------------------------------------------------------------------
 constexpr int kTbWarps = 4;
-constexpr int kTbCols = 40;   // 32 + G - 1 <= 39 tile columns
+constexpr int kTbX = 42;      // tile columns: halo + 32 + G - 1 (<= 40) -> padded
+constexpr int16_t kNeg16 = -16384;  // boundary "-inf": below -open - ext for open <= 16383
 
 struct TbSmem {
-  uint8_t code[32][32];
-  uint8_t bcode[kTbCols], braw[kTbCols];
-  uint8_t araw[32];
+  int16_t H[33][kTbX], E[33][kTbX], F[33][kTbX];  // row 0 / col 0 = halo
+  uint8_t bcode[kTbX], braw[kTbX];
+  uint8_t acode[32], araw[32];
 };
 
 __device__ __forceinline__ int32_t lo16(uint32_t x) { return (int32_t)(int16_t)(x & 0xFFFFu); }
@@ -754,7 +757,7 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
   const int t0 = g * CL.G;
   const int t1 = min(t0 + CL.G, 32) - 1;
   trow0 = strip * 32 * R + t0 * R;
-  const int cmin = 32 * w - t1;
+  const int cmin = 32 * w - t1;              // tile column index x = c - cmin + 1
   const int width = 32 + (t1 - t0);
   tcmin = cmin;
   __syncwarp();
@@ -764,8 +767,7 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
     T.bcode[x] = ok ? bcodes[c] : (uint8_t)kPad;
     T.braw[x] = ok ? braw[c] : (uint8_t)0;
   }
-  // the walk enters this tile at (rho_in, kap_in) and only moves up/left:
-  // rows below it and columns right of it are never read
+  // the walk enters at (rho_in, kap_in) and only moves up/left
   const int qmax = rho_in - trow0;
   const int q = lane;
   const bool row_ok = q <= qmax;
@@ -773,9 +775,12 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
   const int rho = trow0 + q;
   const bool real_row = row_ok & (rho < m);
   const int acode = real_row ? acodes[rho] : kPad;
-  if (row_ok) T.araw[q] = real_row ? araw[rho] : (uint8_t)0;
+  if (row_ok) {
+    T.acode[q] = (uint8_t)acode;
+    T.araw[q] = real_row ? araw[rho] : (uint8_t)0;
+  }
   const uint32_t *sbase = ck + (uint64_t)strip * CL.strip_words;
-  int32_t Ho = -OPEN, E = kNegInf, hoUpPrevT = -OPEN, FbotT = kNegInf;
+  int32_t Ho = -OPEN, E = kNeg16, hoUpPrevT = -OPEN, FbotT = kNeg16;
   if (w > 0 && row_ok) {
     const uint32_t *wd = sbase + (uint64_t)w * 32 * (R + 1) + tq;
     const uint32_t x = wd[32 * rq], y = wd[32 * R];
@@ -784,12 +789,16 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
     hoUpPrevT = lo16(y);
     FbotT = hi16(y);
   }
-  int32_t outHo = Ho, outF = (rq == R - 1) ? FbotT : kNegInf;
-  const int32_t hoAbove = __shfl_up_sync(0xffffffffu, Ho, 1);
-  int32_t prevTop = (rq == 0) ? hoUpPrevT : hoAbove;
-  // top input of tile row 0 for its 32 columns, one per lane, packed (Ho, F)
-  uint32_t topv = 0xC0000000u | ((uint32_t)(-OPEN) & 0xFFFFu);  // (F = -16384, Ho = -open)
+  // halo: this row's left boundary (column c_lo - 1) and, for the first row of
+  // each forward lane, the diagonal above it (column c_lo - 1 of the row above)
+  const int x0 = t1 - tq;                    // tile column of c_lo(q) - 1
+  if (row_ok) {
+    T.H[q + 1][x0] = (int16_t)(Ho + OPEN);
+    if (rq == 0) T.H[q][x0] = (int16_t)(hoUpPrevT + OPEN);
+  }
+  // top halo row: H of the row above the tile at columns c_lo(t0) .. +31
   {
+    uint32_t topv = ((uint32_t)(uint16_t)kNeg16 << 16) | ((uint32_t)(-OPEN) & 0xFFFFu);
     const uint32_t *toprow = nullptr;
     int tsrc = 0;
     if (t0 > 0) {
@@ -803,35 +812,34 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
       const int idx = 32 * w - t0 + lane + tsrc;
       if (idx >= 0) topv = toprow[idx];
     }
+    T.H[0][t1 - t0 + 1 + lane] = (int16_t)(lo16(topv) + OPEN);
+    T.F[0][t1 - t0 + 1 + lane] = (int16_t)hi16(topv);
   }
+  int32_t outHo = Ho, outF = (rq == R - 1) ? FbotT : (int32_t)kNeg16;
+  const int32_t hoAbove = __shfl_up_sync(0xffffffffu, Ho, 1);
+  int32_t prevTop = (rq == 0) ? hoUpPrevT : hoAbove;
   const int vstart = q - q / R;
   const int vlast = min(qmax - qmax / R + 31, kap_in - (32 * w - t0) + qmax);
+  __syncwarp();
   for (int v = 0; v <= vlast; ++v) {
     int32_t topHo = __shfl_up_sync(0xffffffffu, outHo, 1);
     int32_t topF = __shfl_up_sync(0xffffffffu, outF, 1);
-    const uint32_t tv = __shfl_sync(0xffffffffu, topv, v & 31);
-    if (q == 0) {
-      topHo = lo16(tv);
-      topF = hi16(tv);
-      if (topF == -16384) topF = kNegInf;  // unpacked boundary sentinel
+    const int c = 32 * w - t0 + v - q;
+    const int x = c - cmin + 1;
+    if (q == 0) {  // row 0 reads the staged top halo
+      const int xx = min(max(x, 0), kTbX - 1);
+      topHo = (int32_t)T.H[0][xx] - OPEN;
+      topF = T.F[0][xx];
     }
     const bool active = row_ok & (v >= vstart) & (v <= vstart + 31);
     if (active) {
-      const int c = 32 * w - t0 + v - q;
-      const int32_t sc = smat[acode * kCodes + T.bcode[c - cmin]];
-      const int32_t ee = E - EXT, hl = Ho;
-      const int32_t e = max(ee, hl);
-      const int32_t ff = topF - EXT;
-      const int32_t f = max(ff, topHo);
-      const int32_t D = prevTop + sc + OPEN;
-      const int32_t t = __vimax_s32_relu(D, e);
-      const int32_t h = max(t, f);
-      // see box_step: decide from the max's inputs, never `x == max(..)`
-      const bool zero = (D <= 0) & (e <= 0) & (f <= 0);
-      const bool dg = (D >= e) & (D >= f);
-      const bool up = f >= t;
-      const uint32_t src = zero ? 0u : (dg ? 1u : (up ? 2u : 3u));
-      T.code[q][v - vstart] = (uint8_t)(src | (topHo >= ff ? 4u : 0u) | (hl >= ee ? 8u : 0u));
+      const int32_t sc = smat[acode * kCodes + T.bcode[x - 1]];
+      const int32_t e = max(E - EXT, Ho);
+      const int32_t f = max(topF - EXT, topHo);
+      const int32_t h = __vimax3_s32_relu(prevTop + sc + OPEN, e, f);
+      T.H[q + 1][x] = (int16_t)h;
+      T.E[q + 1][x] = (int16_t)e;
+      T.F[q + 1][x] = (int16_t)f;
       E = e;
       Ho = h - OPEN;
       outHo = Ho;
@@ -874,7 +882,7 @@ k_tb(KArgs A, int stage, int cls) {
       const int rho = i - 1, kap = j - 1;
       // fast path: still inside the replayed part of the current tile
       int q = rho - trow0;
-      int u = kap - (cw * 32 - (cg * CL.G + q / R));
+      const int u = kap - (cw * 32 - (cg * CL.G + q / R));
       if (!(cs >= 0 && q >= 0 && q <= tqmax && u >= 0 && u < 32)) {
         const int strip = rho / (32 * R);
         const int t = (rho - strip * 32 * R) / R;
@@ -885,24 +893,31 @@ k_tb(KArgs A, int stage, int cls) {
         cs = strip; cg = g; cw = w;
         q = rho - trow0;
         tqmax = q;
-        u = kap - (32 * w - t);
       }
-      const uint32_t nib = T.code[q][u];
-      if (state == 0) {
-        const uint32_t src = nib & 3u;
-        if (src == 0u) break;
-        if (src == 1u) {
-          matches += T.araw[q] == T.braw[kap - tcmin];
+      const int x = kap - tcmin + 1;
+      const int32_t h = T.H[q + 1][x];
+      if (state == 0) {                       // align.py:137-151
+        if (h == 0) break;
+        const int32_t s = smat[T.acode[q] * kCodes + T.bcode[x - 1]];
+        if (h == (int32_t)T.H[q][x - 1] + s) {
+          matches += T.araw[q] == T.braw[x - 1];
           ++aln; --i; --j;
+        } else if (h == (int32_t)T.F[q + 1][x]) {
+          state = 1;
+        } else if (h == (int32_t)T.E[q + 1][x]) {
+          state = 2;
         } else {
-          state = (int)src - 1;
+          lost = true;
+          break;
         }
-      } else if (state == 1) {
+      } else if (state == 1) {                // align.py:152-160
+        const bool close = (int32_t)T.F[q + 1][x] == (int32_t)T.H[q][x] - OPEN;
         ++aln; --i;
-        if (nib & 4u) state = 0;
-      } else {
+        if (close) state = 0;
+      } else {                                // align.py:161-169
+        const bool close = (int32_t)T.E[q + 1][x] == (int32_t)T.H[q + 1][x - 1] - OPEN;
         ++aln; --j;
-        if (nib & 8u) state = 0;
+        if (close) state = 0;
       }
     }
     if (lane == 0) {
