@@ -895,14 +895,34 @@ k_tb(KArgs A, int stage, int cls) {
         tqmax = q;
       }
       const int x = kap - tcmin + 1;
-      const int32_t h = T.H[q + 1][x];
+      // first tile column of tile row qq (its left halo is at x_first - 1)
+      const int t0 = cg * CL.G, tspan = min(t0 + CL.G, 32) - 1 - t0;
       if (state == 0) {                       // align.py:137-151
+        // Resolve a diagonal run 32 cells at a time: lane k checks cell
+        // (q-k, x-k); the run continues while each cell is an H-state diagonal
+        // move (h != 0 and h == H[diag] + s) inside the replayed tile.
+        const int qq = q - lane, xx = x - lane;
+        bool ok = (qq >= 0) && (kap - lane >= 0);
+        ok = ok && (xx >= tspan - qq / R + 1);
+        bool dg = false, mt = false;
+        if (ok) {
+          const int32_t hk = T.H[qq + 1][xx];
+          const int32_t sk = smat[T.acode[qq] * kCodes + T.bcode[xx - 1]];
+          dg = (hk != 0) && (hk == (int32_t)T.H[qq][xx - 1] + sk);
+          mt = T.araw[qq] == T.braw[xx - 1];
+        }
+        const uint32_t run_mask = __ballot_sync(0xffffffffu, dg);
+        const uint32_t mt_mask = __ballot_sync(0xffffffffu, mt);
+        const int run = (run_mask == 0xffffffffu) ? 32 : __ffs(~run_mask) - 1;
+        if (run > 0) {
+          const uint32_t sel = run == 32 ? 0xffffffffu : ((1u << run) - 1u);
+          matches += __popc(mt_mask & sel);
+          aln += run; i -= run; j -= run;
+          continue;
+        }
+        const int32_t h = T.H[q + 1][x];
         if (h == 0) break;
-        const int32_t s = smat[T.acode[q] * kCodes + T.bcode[x - 1]];
-        if (h == (int32_t)T.H[q][x - 1] + s) {
-          matches += T.araw[q] == T.braw[x - 1];
-          ++aln; --i; --j;
-        } else if (h == (int32_t)T.F[q + 1][x]) {
+        if (h == (int32_t)T.F[q + 1][x]) {
           state = 1;
         } else if (h == (int32_t)T.E[q + 1][x]) {
           state = 2;
@@ -910,14 +930,30 @@ k_tb(KArgs A, int stage, int cls) {
           lost = true;
           break;
         }
-      } else if (state == 1) {                // align.py:152-160
-        const bool close = (int32_t)T.F[q + 1][x] == (int32_t)T.H[q][x] - OPEN;
-        ++aln; --i;
-        if (close) state = 0;
-      } else {                                // align.py:161-169
-        const bool close = (int32_t)T.E[q + 1][x] == (int32_t)T.H[q + 1][x - 1] - OPEN;
-        ++aln; --j;
-        if (close) state = 0;
+      } else if (state == 1) {                // align.py:152-160: vertical gap run
+        const int qq = q - lane;
+        const bool ok = (qq >= 0) && (x >= tspan - qq / R + 1);
+        const bool close =
+            ok && ((int32_t)T.F[qq + 1][x] == (int32_t)T.H[qq][x] - OPEN);
+        const uint32_t cm = __ballot_sync(0xffffffffu, close);
+        const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+        const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
+        int steps;
+        if (cm) { steps = __ffs(cm); state = 0; }
+        else steps = nvalid;
+        aln += steps; i -= steps;
+      } else {                                // align.py:161-169: horizontal gap run
+        const int xx = x - lane;
+        const bool ok = (kap - lane >= 0) && (xx >= tspan - q / R + 1);
+        const bool close =
+            ok && ((int32_t)T.E[q + 1][xx] == (int32_t)T.H[q + 1][xx - 1] - OPEN);
+        const uint32_t cm = __ballot_sync(0xffffffffu, close);
+        const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+        const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
+        int steps;
+        if (cm) { steps = __ffs(cm); state = 0; }
+        else steps = nvalid;
+        aln += steps; j -= steps;
       }
     }
     if (lane == 0) {
