@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "sw_kernels.cuh"
+#include "sw_packed.cuh"
 
 using namespace pastis;
 
@@ -68,6 +69,7 @@ typedef void (*KernelFn)(KArgs, int, int);
 struct KernelInfo {
   KernelFn fn;
   int grid;
+  int smem;
 };
 
 struct DeviceCtx {
@@ -102,6 +104,20 @@ int setup_kernel(K fn, int sms, KernelInfo &ki, int &max_warps) {
 }
 
 template <typename K>
+int setup_packed(K fn, int sms, int smem, KernelInfo &ki, int &max_warps) {
+  CU(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int nb = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)fn, kWarpsPerBlockP * 32,
+                                                   smem));
+  if (nb < 1) return fail(SW_ECUDA, "packed kernel cannot be resident");
+  ki.fn = (KernelFn)fn;
+  ki.grid = nb * sms;
+  ki.smem = smem;
+  max_warps = std::max(max_warps, ki.grid * kWarpsPerBlockP);
+  return SW_OK;
+}
+
+template <typename K>
 int setup_tb(K fn, int sms, KernelInfo &ki) {
   int nb = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)fn, kTbWarps * 32, 0));
@@ -121,7 +137,7 @@ int setup_classes(DeviceCtx *c) {
     if (rc) return rc;
     rc = setup_kernel(k_box<R, false>, c->sms, c->box[C], c->max_warps);
     if (rc) return rc;
-    rc = setup_kernel(k_score<R, 0, false, true>, c->sms, c->ckpt[C], c->max_warps);
+    rc = setup_packed(k_score_packed<R>, c->sms, smem_packed(R), c->ckpt[C], c->max_warps);
     if (rc) return rc;
     rc = setup_tb(k_tb<R>, c->sms, c->tb[C]);
     if (rc) return rc;
@@ -232,6 +248,15 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   A.n_pairs = n_pairs;
   A.open_ = prm->gap_open;
   A.ext = prm->gap_extend;
+  int smin = 127, smax = -128;
+  for (int i = 0; i < 625; ++i) {
+    smin = std::min(smin, (int)prm->matrix[i]);
+    smax = std::max(smax, (int)prm->matrix[i]);
+  }
+  A.prof_lo = std::min(smin - 1, -1);           // virtual cells score prof_lo < 0
+  A.bias16 = prm->gap_open + prm->gap_extend + 128;
+  // packed forward pass needs u8 profile bytes < 128
+  const bool packed_ok = smax - A.prof_lo <= 127;
 
   CU(cudaEventRecord(c->ev[0], s));
   {
@@ -243,12 +268,12 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     // PASTIS_SW_TRACEBACK=box forces the reverse-pass + box traceback for every
     // pair (A/B comparisons); default: checkpoint + tile replay for pairs
     // up to kFusedMaxCells cells.
-    static const int allow_ckpt = [] {
+    static const int env_ckpt = [] {
       const char *e = getenv("PASTIS_SW_TRACEBACK");
       return (e && strcmp(e, "box") == 0) ? 0 : 1;
     }();
     k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(A, (unsigned long long *)c->stats.p,
-                                                                allow_ckpt);
+                                                                env_ckpt && packed_ok);
     ++launches;
     CU(cudaGetLastError());
   }
@@ -286,8 +311,8 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   const double h2 = now_ms();
 
   CU(cudaEventRecord(c->ev[1], s));
-  for (int cls = 0; cls < kNumClasses; ++cls) {  // short/medium pairs: forward + checkpoints
-    c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 6, cls);
+  for (int cls = 0; cls < kNumClasses; ++cls) {  // short/medium pairs: packed forward + checkpoints
+    c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, s>>>(A, 6, cls);
     ++launches;
   }
   for (int cls = 0; cls < kNumClasses; ++cls) {  // long pairs: score-only forward

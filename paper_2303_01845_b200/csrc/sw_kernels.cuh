@@ -57,7 +57,7 @@ __host__ __device__ inline int class_of(int m) {
 }
 __host__ __device__ constexpr int box_lane_bytes(int R) { return R <= 4 ? 2 : R <= 8 ? 4 : 8; }
 
-enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4 };
+enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4, kFlagNeedJ = 8 };
 
 struct PairState {         // per-pair scratch between the passes (48 B)
   int32_t best, i_end, j_end, flags;
@@ -82,6 +82,8 @@ struct KArgs {
   uint64_t pool_cap;
   unsigned long long *pool_top;
   int32_t open_, ext;
+  int32_t bias16;           // B: checkpoint values are stored as u16 (v + B)
+  int32_t prof_lo;          // packed profile stores s - prof_lo (0..127); PAD -> 0
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -176,8 +178,9 @@ struct BoundaryReader {
 // Checkpoints written by the forward pass (short/medium pairs) so that the
 // traceback can replay only the 32-column tiles its path crosses:
 //  * column checkpoints: at the end of every 32-step window w-1 each lane
-//    stores its state entering window w: (Ho_r, E_r) for its R rows plus
-//    (hoUpPrev, F_bot) -> R+1 words of two int16 (unscaled values);
+//    stores its state entering window w: (Ho_r, E_r) for its R rows,
+//    (hoUpPrev, F_bot), and the running row maxima -> 2R+1 words, values
+//    as biased u16 (v + B);
 //  * row checkpoints: "boundary" lanes (the last lane of each group of
 //    G = 32/R lanes, and lane 31) store their bottom-row (Ho, F) every step.
 // Per strip: [window][word (R+1)][lane] words (coalesced stores), then
@@ -193,7 +196,7 @@ __host__ __device__ inline CkLayout ck_layout(int R, int n) {
   L.nb = (32 + L.G - 1) / L.G;
   L.nwin = (n + 31 + 31) / 32;
   L.spad = L.nwin * 32;
-  L.col_words = (uint32_t)L.nwin * 32u * (uint32_t)(R + 1);
+  L.col_words = (uint32_t)L.nwin * 32u * (uint32_t)(2 * R + 1);
   L.strip_words = L.col_words + (uint32_t)L.nb * (uint32_t)L.spad;
   return L;
 }
@@ -744,16 +747,17 @@ struct TbSmem {
   uint8_t acode[32], araw[32];
 };
 
-__device__ __forceinline__ int32_t lo16(uint32_t x) { return (int32_t)(int16_t)(x & 0xFFFFu); }
-__device__ __forceinline__ int32_t hi16(uint32_t x) { return (int32_t)(int16_t)(x >> 16); }
+// checkpoint words hold two biased u16 values (v + B)
+__device__ __forceinline__ int32_t ulo(uint32_t x, int32_t B) { return (int32_t)(x & 0xFFFFu) - B; }
+__device__ __forceinline__ int32_t uhi(uint32_t x, int32_t B) { return (int32_t)(x >> 16) - B; }
 
 template <int R>
 __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const uint32_t *ck,
                                           const CkLayout &CL, int strip, int g, int w, int m,
                                           int n, const uint8_t *acodes, const uint8_t *bcodes,
                                           const uint8_t *araw, const uint8_t *braw, int lane,
-                                          int32_t OPEN, int32_t EXT, int &trow0, int &tcmin,
-                                          const int rho_in, const int kap_in) {
+                                          int32_t OPEN, int32_t EXT, int32_t B, int &trow0,
+                                          int &tcmin, const int rho_in, const int kap_in) {
   const int t0 = g * CL.G;
   const int t1 = min(t0 + CL.G, 32) - 1;
   trow0 = strip * 32 * R + t0 * R;
@@ -782,12 +786,12 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
   const uint32_t *sbase = ck + (uint64_t)strip * CL.strip_words;
   int32_t Ho = -OPEN, E = kNeg16, hoUpPrevT = -OPEN, FbotT = kNeg16;
   if (w > 0 && row_ok) {
-    const uint32_t *wd = sbase + (uint64_t)w * 32 * (R + 1) + tq;
+    const uint32_t *wd = sbase + (uint64_t)w * 32 * (2 * R + 1) + tq;
     const uint32_t x = wd[32 * rq], y = wd[32 * R];
-    Ho = lo16(x);
-    E = hi16(x);
-    hoUpPrevT = lo16(y);
-    FbotT = hi16(y);
+    Ho = ulo(x, B);
+    E = uhi(x, B);
+    hoUpPrevT = ulo(y, B);
+    FbotT = uhi(y, B);
   }
   // halo: this row's left boundary (column c_lo - 1) and, for the first row of
   // each forward lane, the diagonal above it (column c_lo - 1 of the row above)
@@ -798,7 +802,7 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
   }
   // top halo row: H of the row above the tile at columns c_lo(t0) .. +31
   {
-    uint32_t topv = ((uint32_t)(uint16_t)kNeg16 << 16) | ((uint32_t)(-OPEN) & 0xFFFFu);
+    int32_t tHo = -OPEN, tF = kNeg16;
     const uint32_t *toprow = nullptr;
     int tsrc = 0;
     if (t0 > 0) {
@@ -810,10 +814,14 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
     }
     if (toprow) {
       const int idx = 32 * w - t0 + lane + tsrc;
-      if (idx >= 0) topv = toprow[idx];
+      if (idx >= 0) {
+        const uint32_t z = toprow[idx];
+        tHo = ulo(z, B);
+        tF = uhi(z, B);
+      }
     }
-    T.H[0][t1 - t0 + 1 + lane] = (int16_t)(lo16(topv) + OPEN);
-    T.F[0][t1 - t0 + 1 + lane] = (int16_t)hi16(topv);
+    T.H[0][t1 - t0 + 1 + lane] = (int16_t)(tHo + OPEN);
+    T.F[0][t1 - t0 + 1 + lane] = (int16_t)tF;
   }
   int32_t outHo = Ho, outF = (rq == R - 1) ? FbotT : (int32_t)kNeg16;
   const int32_t hoAbove = __shfl_up_sync(0xffffffffu, Ho, 1);
@@ -859,22 +867,53 @@ k_tb(KArgs A, int stage, int cls) {
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   TbSmem &T = tsm[warp];
-  const int32_t OPEN = A.open_, EXT = A.ext;
+  const int32_t OPEN = A.open_, EXT = A.ext, Bias = A.bias16;
   for (;;) {
     const int64_t k = next_item(A, stage, cls, lane);
     if (k < 0) break;
     const sw_pair_t p = A.pairs[k];
     PairState *st = A.st + k;
     const int m = (int)p.a_len, n = (int)p.b_len;
-    const CkLayout CL = ck_layout(R, n);
+    const CkLayout CL = ck_layout(R, st->box_n);   // layout of the forward pass's checkpoints
     const uint32_t *ck = reinterpret_cast<const uint32_t *>(A.pool + st->code_off);
     const uint8_t *acodes = A.codes + p.a_off, *bcodes = A.codes + p.b_off;
     const uint8_t *araw = A.raw + p.a_off, *braw = A.raw + p.b_off;
-    const int i_end = st->i_end, j_end = st->j_end;
-    int i = i_end + 1, j = j_end + 1, state = 0, matches = 0, aln = 0;
+    const int i_end = st->i_end;
+    int j_end = st->j_end;
     int cs = -1, cg = -1, cw = -1, trow0 = 0, tcmin = 0, tqmax = -1;
-    bool lost = false;
+    if (st->flags & kFlagNeedJ) {
+      // The packed forward pass knows best and i_end only.  j_end = first
+      // column of row i_end with H == best: the per-window running row maxima
+      // in the checkpoints give its window w*; replaying that tile gives the
+      // column (align.py:124 row-major-first end cell).
+      const int best = st->best;
+      const int strip = i_end / (32 * R);
+      const int t = (i_end - strip * 32 * R) / R, r = i_end - strip * 32 * R - t * R;
+      const uint32_t *rmcol = ck + (uint64_t)strip * CL.strip_words + 32ull * (R + 1 + r) + t;
+      int wstar = CL.nwin - 1;
+      for (int w0 = 1; w0 < CL.nwin; w0 += 32) {
+        const int w = w0 + lane;
+        bool hit = false;
+        if (w < CL.nwin) hit = (int32_t)(rmcol[(uint64_t)w * 32 * (2 * R + 1)] & 0xFFFFu) - Bias >= best;
+        const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+        if (hm) { wstar = w0 + __ffs(hm) - 1 - 1; break; }
+      }
+      const int g = t / CL.G;
+      const int kap_hi = min(32 * wstar - t + 31, n - 1);
+      tb_replay<R>(T, smat, ck, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+                   EXT, Bias, trow0, tcmin, i_end, kap_hi);
+      cs = strip; cg = g; cw = wstar;
+      const int q = i_end - trow0;
+      tqmax = q;
+      const int c = 32 * wstar - t + lane;
+      const bool hit = (c >= 0) && (c <= kap_hi) && ((int32_t)T.H[q + 1][c - tcmin + 1] >= best);
+      const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+      j_end = hm ? 32 * wstar - t + __ffs(hm) - 1 : -1;
+    }
+    int i = i_end + 1, j = j_end + 1, state = 0, matches = 0, aln = 0;
+    bool lost = j_end < 0;
     for (;;) {
+      if (lost) break;
       if (i == 0 || j == 0) {
         lost = state != 0;
         break;
@@ -889,7 +928,7 @@ k_tb(KArgs A, int stage, int cls) {
         const int g = t / CL.G;
         const int w = (kap + t) >> 5;
         tb_replay<R>(T, smat, ck, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
-                     EXT, trow0, tcmin, rho, kap);
+                     EXT, Bias, trow0, tcmin, rho, kap);
         cs = strip; cg = g; cw = w;
         q = rho - trow0;
         tqmax = q;
@@ -964,6 +1003,7 @@ k_tb(KArgs A, int stage, int cls) {
       r.matches = matches; r.aln_len = aln;
       r.status = lost ? SW_STATUS_INTERNAL : SW_STATUS_OK;
       A.out[k] = r;
+      st->j_end = j_end;
       st->flags |= kFlagDone;
     }
   }

@@ -1,0 +1,369 @@
+// sw_packed.cuh -- K1p: the packed forward pass (two pairs per warp).
+//
+// Same recurrence and wavefront as k_score<FWD> (align.py:103-121), but each
+// 32-bit register holds the same cell of TWO pairs (pair A in the low half,
+// pair B in the high half) as biased unsigned 16-bit values v + B, with
+// B = open + ext + 128.  Measured on B200 (profiles/r01/mix2.txt): plain
+// VIMNMX (s32 or u16x2) issues at full rate on the ALU pipe and co-issues with
+// IMAD (FMA pipe), while the fused DPX ops issue at half rate.  So every add
+// is an IMAD/IADD3 on whole words (the bias keeps both halves in [0, 65535],
+// no borrow crosses a half) and every max is a VIMNMX.U16x2:
+//   E  = max(E - ext, Ho_left)          IMAD + VIMNMX
+//   F  = max(F - ext, Ho_up)            IMAD + VIMNMX
+//   D  = Ho_diag + u + (open + lo)      IADD3  (u = s - lo, 0..127, u8 profile)
+//   h  = max(D, E, F, B)                3 VIMNMX   (B = biased zero: local floor)
+//   Ho = h - open                       IMAD
+//   rowmax = max(rowmax, h)             VIMNMX
+// = ~9 ALU-pipe cycles per 2 cells vs ~10 per cell for the scaled-int32 K1.
+// The score pair comes from the two pairs' int8 profiles with one PRMT (the
+// sign-replicate selector of a byte with msb 0 yields the zero high byte).
+// Per-row maxima give best and i_end (first row reaching best); j_end is found
+// by the traceback kernel from per-window row maxima stored in the column
+// checkpoints (k_tb).  Values are exact while every biased value stays below
+// 65535 - 128; a warp that gets near that re-runs both pairs in the wide path.
+#pragma once
+#include "sw_kernels.cuh"
+
+namespace pastis {
+
+constexpr int kWarpsPerBlockP = 4;
+constexpr int kStageBytesP = 2 * 17 * 8 * 4;     // two pairs x (16 boundaries + dummy) x 8 steps
+constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs
+constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
+
+// u8 profile of one pair: part 0 = [code][lane][P0] (P0 = 4 or 8 bytes),
+// part 1 = [code][lane][P1] for the remaining rows (R = 10 -> 8 + 2 bytes).
+__host__ __device__ constexpr int prof_p0(int R) { return R <= 4 ? 4 : 8; }
+__host__ __device__ constexpr int prof_p1(int R) { return R <= 8 ? 0 : (R <= 10 ? 2 : (R <= 12 ? 4 : 8)); }
+__host__ __device__ constexpr int prof_bytes_p(int R) { return kCodes * 32 * (prof_p0(R) + prof_p1(R)); }
+__host__ __device__ constexpr int warp_bytes_p(int R) {
+  return (2 * prof_bytes_p(R) + kStageBytesP + kRingBytes + 15) / 16 * 16;
+}
+__host__ __device__ constexpr int smem_packed(int R) { return kMatBytes + kWarpsPerBlockP * warp_bytes_p(R); }
+
+__device__ __forceinline__ uint32_t vmax2u(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t splat16(uint32_t v) { return (v & 0xFFFFu) * 0x10001u; }
+
+// u8 profile (s - lo) for rows row0+lane*R .. +R-1 of one pair; PAD -> 0.
+template <int R>
+__device__ __forceinline__ void build_profile_u8(uint8_t *prof, const int8_t *mat, const View &rows,
+                                                 int m, int row0, int lane, int lo) {
+  constexpr int P0 = prof_p0(R), P1 = prof_p1(R);
+  int arow[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int x = row0 + lane * R + r;
+    arow[r] = x < m ? rows.at(x) : kPad;
+  }
+#pragma unroll 2
+  for (int code = 0; code < kCodes; ++code) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int a = arow[r];
+      const int v = (a == kPad || code == kPad) ? 0 : (int)mat[code * kCodes + a] - lo;
+      w[r >> 2] |= (uint32_t)v << (8 * (r & 3));
+    }
+    uint8_t *p0 = prof + (code * 32 + lane) * P0;
+    if (P0 == 4) *reinterpret_cast<uint32_t *>(p0) = w[0];
+    else *reinterpret_cast<uint2 *>(p0) = make_uint2(w[0], w[1]);
+    if (P1 > 0) {
+      uint8_t *p1 = prof + kCodes * 32 * P0 + (code * 32 + lane) * P1;
+      if (P1 == 2) *reinterpret_cast<uint16_t *>(p1) = (uint16_t)w[2];
+      else if (P1 == 4) *reinterpret_cast<uint32_t *>(p1) = w[2];
+      else *reinterpret_cast<uint2 *>(p1) = make_uint2(w[2], w[3]);
+    }
+  }
+}
+
+// this lane's R profile bytes for column code `code`, as 4 words (rows 4k..4k+3)
+template <int R>
+__device__ __forceinline__ uint4 load_profile_u8(const uint8_t *prof, int code, int lane) {
+  constexpr int P0 = prof_p0(R), P1 = prof_p1(R);
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  const uint8_t *p0 = prof + (code * 32 + lane) * P0;
+  if (P0 == 4) {
+    v.x = *reinterpret_cast<const uint32_t *>(p0);
+  } else {
+    const uint2 a = *reinterpret_cast<const uint2 *>(p0);
+    v.x = a.x;
+    v.y = a.y;
+  }
+  if (P1 > 0) {
+    const uint8_t *p1 = prof + kCodes * 32 * P0 + (code * 32 + lane) * P1;
+    if (P1 == 2) v.z = *reinterpret_cast<const uint16_t *>(p1);
+    else if (P1 == 4) v.z = *reinterpret_cast<const uint32_t *>(p1);
+    else {
+      const uint2 b = *reinterpret_cast<const uint2 *>(p1);
+      v.z = b.x;
+      v.w = b.y;
+    }
+  }
+  return v;
+}
+
+// byte k of a (low half) and byte k of b (high half), zero-extended:
+// selector nibbles {k, k|8, 4+k, (4+k)|8}; bytes are < 128 so the
+// sign-replicated bytes are 0.
+__device__ __forceinline__ uint32_t sel_pair(int k) {
+  return (uint32_t)k | ((uint32_t)(k | 8) << 4) | ((uint32_t)(4 + k) << 8) |
+         ((uint32_t)((4 + k) | 8) << 12);
+}
+
+template <int R>
+struct PackedLane {
+  uint32_t Ho[R], E[R], rm[R];
+  uint32_t hoUpPrev, botHo, botF;
+};
+
+struct PackedPair {        // one of the two pairs a warp carries
+  int64_t k;               // pair index (-1: none)
+  int m, n;
+  View rows, cols;
+  uint32_t *ck;            // checkpoint region (nullptr: no room -> box path)
+  unsigned long long ck_off;
+};
+
+template <int R>
+__global__ void __launch_bounds__(kWarpsPerBlockP * 32, 3)
+k_score_packed(KArgs A, int stage, int cls) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int8_t *smat = reinterpret_cast<int8_t *>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t *profA = smem + kMatBytes + warp * warp_bytes_p(R);
+  uint8_t *profB = profA + prof_bytes_p(R);
+  uint32_t *stageA = reinterpret_cast<uint32_t *>(profB + prof_bytes_p(R));
+  uint32_t *stageB = stageA + 17 * 8;
+  uint8_t *ringA = reinterpret_cast<uint8_t *>(stageB + 17 * 8);
+  uint8_t *ringB = ringA + 128;
+  load_matrix(smat, A.mat);
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlockP + warp;
+  int2 *bnd = A.bnd + gwarp * A.bnd_stride;
+  const uint32_t Bs = (uint32_t)A.bias16;
+  const uint32_t BB = splat16(Bs);
+  const uint32_t OPEN2 = splat16((uint32_t)A.open_);
+  const uint32_t EXT2 = splat16((uint32_t)A.ext);
+  const uint32_t NEG2 = EXT2;                          // biased "-inf": E/F - ext == 0
+  const uint32_t HO0 = BB - OPEN2;                     // biased H - open for H == 0
+  const int32_t K2 = (A.open_ + A.prof_lo) * 0x10001;  // D = Ho_diag + u + K2
+  const int lo = A.prof_lo;
+  for (;;) {
+    // two consecutive work items per warp
+    uint32_t pos = 0;
+    if (lane == 0) pos = atomicAdd(&A.ctrs[kStages * kNumClasses + stage * kNumClasses + cls], 2u);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const uint32_t cnt = *(volatile uint32_t *)&A.ctrs[stage * kNumClasses + cls];
+    if (pos >= cnt) break;
+    PackedPair P[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t idx = pos + h;
+      P[h].k = idx < cnt ? (int64_t)list_of(A, stage, cls)[idx] : -1;
+      if (P[h].k >= 0) {
+        const sw_pair_t p = A.pairs[P[h].k];
+        P[h].m = (int)p.a_len;
+        P[h].n = (int)p.b_len;
+        P[h].rows = View{A.codes + p.a_off, 1};
+        P[h].cols = View{A.codes + p.b_off, 1};
+      } else {
+        P[h].m = 0;
+        P[h].n = 0;
+        P[h].rows = View{A.codes, 1};
+        P[h].cols = View{A.codes, 1};
+      }
+      P[h].ck = nullptr;
+      P[h].ck_off = 0;
+    }
+    const int m = max(P[0].m, P[1].m), n = max(P[0].n, P[1].n);
+    const int nstrips = (m + 32 * R - 1) / (32 * R);
+    const CkLayout CL = ck_layout(R, n);
+    const uint64_t bytes = (uint64_t)nstrips * CL.strip_words * 4ull;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (P[h].k < 0) continue;
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(A.pool_top, (unsigned long long)bytes);
+      off = __shfl_sync(0xffffffffu, off, 0);
+      if (off + bytes <= A.pool_cap) {
+        P[h].ck = reinterpret_cast<uint32_t *>(A.pool + off);
+        P[h].ck_off = off;
+      }
+    }
+    uint64_t keyA = 0ull, keyB = 0ull;
+    uint32_t vmax2 = 0u;
+    for (int strip = 0; strip < nstrips; ++strip) {
+      const int row0 = strip * 32 * R;
+      __syncwarp();
+      build_profile_u8<R>(profA, smat, P[0].rows, P[0].m, row0, lane, lo);
+      build_profile_u8<R>(profB, smat, P[1].rows, P[1].m, row0, lane, lo);
+      __syncwarp();
+      PackedLane<R> L;
+#pragma unroll
+      for (int r = 0; r < R; ++r) { L.Ho[r] = HO0; L.E[r] = NEG2; L.rm[r] = BB; }
+      L.hoUpPrev = HO0;
+      L.botHo = HO0;
+      L.botF = NEG2;
+      // column-code rings: slot c & 127 holds column c; prefill [-32, 96)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = -32 + 32 * q + lane;
+        ringA[c & 127] = (c >= 0 && c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
+        ringB[c & 127] = (c >= 0 && c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
+      }
+      const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
+      BoundaryReader br;
+      const int2 dflt = make_int2((int32_t)HO0, (int32_t)NEG2);
+      if (has_above) br.init(bnd, n, lane, dflt);
+      // checkpoint destinations for this strip
+      uint32_t *colA = P[0].ck ? P[0].ck + (uint64_t)strip * CL.strip_words + lane : nullptr;
+      uint32_t *colB = P[1].ck ? P[1].ck + (uint64_t)strip * CL.strip_words + lane : nullptr;
+      const int b = ck_boundary(lane, CL);
+      const int bslot = (b >= 0 ? b : 16) * kScoreUnroll;   // non-boundary lanes -> dummy row
+      uint4 *flA = nullptr, *flB = nullptr;
+      if (lane < 2 * CL.nb) {
+        if (P[0].ck)
+          flA = reinterpret_cast<uint4 *>(P[0].ck + (uint64_t)strip * CL.strip_words + CL.col_words +
+                                          (uint32_t)(lane >> 1) * CL.spad) + (lane & 1);
+        if (P[1].ck)
+          flB = reinterpret_cast<uint4 *>(P[1].ck + (uint64_t)strip * CL.strip_words + CL.col_words +
+                                          (uint32_t)(lane >> 1) * CL.spad) + (lane & 1);
+      }
+      const int steps = n + 31;
+      __syncwarp();
+      for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
+        if ((s0 & 31) == 0 && s0 > 0) {    // refill ring slots for columns s0+64 .. s0+95
+          const int c = s0 + 64 + lane;
+          ringA[c & 127] = (c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
+          ringB[c & 127] = (c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < kScoreUnroll; ++q) {
+          const int s = s0 + q;
+          const int c = s - lane;
+          const uint4 pa = load_profile_u8<R>(profA, ringA[c & 127], lane);
+          const uint4 pb = load_profile_u8<R>(profB, ringB[c & 127], lane);
+          uint32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
+          uint32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
+          if (has_above) {
+            const int2 bv = br.get(bnd, s, n, lane, dflt);
+            if (lane == 0) { upHo = (uint32_t)bv.x; upF = (uint32_t)bv.y; }
+          } else if (lane == 0) {
+            upHo = HO0; upF = NEG2;
+          }
+          uint32_t diag = L.hoUpPrev;
+          L.hoUpPrev = upHo;
+          uint32_t F = upF, hoUp = upHo;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const uint32_t u2 = prmt(word_of(pa, r), word_of(pb, r), sel_pair(r & 3));
+            L.E[r] = vmax2u(L.E[r] - EXT2, L.Ho[r]);
+            F = vmax2u(F - EXT2, hoUp);
+            const uint32_t D = diag + u2 + (uint32_t)K2;
+            const uint32_t h = vmax2u(vmax2u(vmax2u(D, L.E[r]), F), BB);
+            diag = L.Ho[r];
+            L.Ho[r] = h - OPEN2;
+            hoUp = L.Ho[r];
+            L.rm[r] = vmax2u(L.rm[r], h);
+          }
+          L.botHo = hoUp;
+          L.botF = F;
+          if (has_below && lane == 31 && c >= 0 && c < n) bnd[c] = make_int2((int32_t)hoUp, (int32_t)F);
+          stageA[bslot + q] = prmt(hoUp, F, 0x5410u);
+          stageB[bslot + q] = prmt(hoUp, F, 0x7632u);
+        }
+        __syncwarp();
+        if (flA) flA[s0 / 4] = reinterpret_cast<const uint4 *>(stageA)[lane];
+        if (flB) flB[s0 / 4] = reinterpret_cast<const uint4 *>(stageB)[lane];
+        __syncwarp();
+        // column checkpoint: state entering window w (after step 32w - 1)
+        if (((s0 + kScoreUnroll) & 31) == 0) {
+          const int w = (s0 + kScoreUnroll) >> 5;
+          if (w < CL.nwin) {
+            const uint64_t base = (uint64_t)w * 32 * (2 * R + 1);
+            if (colA) {
+              uint32_t *d = colA + base;
+#pragma unroll
+              for (int r = 0; r < R; ++r) d[32 * r] = prmt(L.Ho[r], L.E[r], 0x5410u);
+              d[32 * R] = prmt(L.hoUpPrev, L.botF, 0x5410u);
+#pragma unroll
+              for (int r = 0; r < R; ++r) d[32 * (R + 1 + r)] = L.rm[r] & 0xFFFFu;
+            }
+            if (colB) {
+              uint32_t *d = colB + base;
+#pragma unroll
+              for (int r = 0; r < R; ++r) d[32 * r] = prmt(L.Ho[r], L.E[r], 0x7632u);
+              d[32 * R] = prmt(L.hoUpPrev, L.botF, 0x7632u);
+#pragma unroll
+              for (int r = 0; r < R; ++r) d[32 * (R + 1 + r)] = L.rm[r] >> 16;
+            }
+          }
+        }
+      }
+      // strip reduction: best and the first row reaching it, per pair
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int x = row0 + lane * R + r;
+        const uint32_t va = L.rm[r] & 0xFFFFu, vb = L.rm[r] >> 16;
+        vmax2 = max(vmax2, max(va, vb));
+        if (x < P[0].m) {
+          const uint64_t kk = ((uint64_t)(va - Bs) << 32) | ((uint64_t)(0xFFFF - x) << 16);
+          keyA = kk > keyA ? kk : keyA;
+        }
+        if (x < P[1].m) {
+          const uint64_t kk = ((uint64_t)(vb - Bs) << 32) | ((uint64_t)(0xFFFF - x) << 16);
+          keyB = kk > keyB ? kk : keyB;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t a2 = __shfl_xor_sync(0xffffffffu, keyA, o);
+      keyA = a2 > keyA ? a2 : keyA;
+      const uint64_t b2 = __shfl_xor_sync(0xffffffffu, keyB, o);
+      keyB = b2 > keyB ? b2 : keyB;
+      vmax2 = max(vmax2, (uint32_t)__shfl_xor_sync(0xffffffffu, vmax2, o));
+    }
+    if (lane == 0) {
+      const bool overflow = vmax2 > kPackedLimit;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (P[h].k < 0) continue;
+        PairState *st = A.st + P[h].k;
+        const uint64_t key = h == 0 ? keyA : keyB;
+        const int32_t best = (int32_t)(key >> 32);
+        const int32_t i_end = 0xFFFF - (int32_t)((key >> 16) & 0xFFFF);
+        st->i0 = 0;
+        st->j0 = 0;
+        if (overflow) {                        // both halves suspect: wide path
+          st->flags = kFlagWide;
+          list_push(A, 3, 0, (uint32_t)P[h].k);
+        } else if (best == 0) {
+          st->best = 0;
+          st->i_end = -1;
+          st->j_end = -1;
+          st->flags = 0;
+        } else if (P[h].ck) {
+          st->best = best;
+          st->i_end = i_end;
+          st->j_end = -1;                      // resolved by k_tb from the checkpoints
+          st->flags = kFlagNeedJ;
+          st->code_off = P[h].ck_off;
+          st->box_cls = cls;
+          st->box_m = m;
+          st->box_n = n;
+          list_push(A, 7, cls, (uint32_t)P[h].k);
+        } else {                               // no checkpoint room: scalar path
+          st->flags = 0;
+          list_push(A, 0, class_of(P[h].m), (uint32_t)P[h].k);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace pastis
