@@ -255,6 +255,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   }
   A.prof_lo = std::min(smin - 1, -1);           // virtual cells score prof_lo < 0
   A.bias16 = prm->gap_open + prm->gap_extend + 128;
+  A.p_bb = (uint32_t)A.bias16 * 0x10001u;
+  A.p_open2 = (uint32_t)prm->gap_open * 0x10001u;
+  A.p_ext2 = (uint32_t)prm->gap_extend * 0x10001u;
+  A.p_ho0 = A.p_bb - A.p_open2;
+  A.p_k2 = (uint32_t)((prm->gap_open + A.prof_lo) * 0x10001);
   // packed forward pass needs u8 profile bytes < 128
   const bool packed_ok = smax - A.prof_lo <= 127;
 
@@ -277,31 +282,19 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     ++launches;
     CU(cudaGetLastError());
   }
-  unsigned long long stats[4] = {0, 0, 0, 0};
-  CU(cudaMemcpyAsync(stats, c->stats.p, 3 * 8, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  const double h1 = now_ms();
-  const uint64_t cells = stats[0];
-  const uint64_t max_b = stats[1];
-  // per-warp boundary rows for multi-strip pairs
-  A.bnd_stride = max_b + 64;
+  // No host round trip before the kernels: the strip-boundary scratch is
+  // sized for the longest supported sequence and the traceback pool is one
+  // large cached allocation (pool overflow falls back to retry rounds).
+  A.bnd_stride = 65000 + 64;
   CU(c->bnd.ensure((size_t)c->max_warps * A.bnd_stride * sizeof(int2)));
   A.bnd = (int2 *)c->bnd.p;
-  // traceback code pool (grow-only; overflow falls back to retry rounds)
-  {
-    // cudaMemGetInfo costs milliseconds: only ask when the pool must grow
-    const size_t want = std::min<size_t>(
-        std::max<size_t>((size_t)(cells * 1.1) + (64ull << 20), 256ull << 20), (size_t)24 << 30);
-    if (c->pool.bytes < want) {
-      size_t free_b = 0, total_b = 0;
-      CU(cudaMemGetInfo(&free_b, &total_b));
-      const size_t cap = std::min<size_t>(want, (size_t)((free_b + c->pool.bytes) * 0.6));
-      if (c->pool.bytes < cap) {
-        c->pool.release();
-        CU(c->pool.ensure(cap));
-      }
-    }
+  if (c->pool.bytes == 0) {
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    const size_t cap = std::min<size_t>((size_t)(free_b * 0.5), (size_t)48 << 30);
+    CU(c->pool.ensure(std::max<size_t>(cap, (size_t)256 << 20)));
   }
+  const double h1 = now_ms();
   A.pool = (uint8_t *)c->pool.p;
   A.pool_cap = c->pool.bytes - 64;  // headroom for the widest vector store
   CU(c->ctrs.ensure(2 * kStages * kNumClasses * 4));
@@ -367,7 +360,9 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     tm->reverse_ms += ev_ms(c->ev[2], c->ev[3]);
     tm->traceback_ms += tb_ms;
     tm->kernel_ms += ev_ms(c->ev[0], c->ev[1]) + ev_ms(c->ev[1], c->ev[3]) + tb_ms;
-    tm->cells += cells;
+    unsigned long long hstats[2] = {0ull, 0ull};
+    CU(cudaMemcpy(hstats, c->stats.p, sizeof(hstats), cudaMemcpyDeviceToHost));
+    tm->cells += hstats[0];
     tm->launches += launches;
     uint32_t h_ctrs[kStages * kNumClasses];
     CU(cudaMemcpy(h_ctrs, c->ctrs.p, sizeof(h_ctrs), cudaMemcpyDeviceToHost));

@@ -84,6 +84,10 @@ struct KArgs {
   int32_t open_, ext;
   int32_t bias16;           // B: checkpoint values are stored as u16 (v + B)
   int32_t prof_lo;          // packed profile stores s - prof_lo (0..127); PAD -> 0
+  // packed (u16x2) constants, precomputed on the host so they live in the
+  // constant bank: B, open, ext splatted to both halves, H-open at H=0, and
+  // the D offset (open + prof_lo) * 0x10001
+  uint32_t p_bb, p_open2, p_ext2, p_ho0, p_k2;
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -1104,21 +1108,46 @@ __global__ void k_encode(const uint8_t *__restrict__ raw, uint8_t *__restrict__ 
     codes[i] = slut[raw[i]];
 }
 
-// Classify pairs for K1 by row count; count cells; reset per-pair state.
+// Classify pairs by row count into work lists (warp-aggregated appends);
+// count cells; reset per-pair state.
 __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= A.n_pairs) return;
-  const sw_pair_t p = A.pairs[k];
-  PairState s;
-  s.best = 0; s.i_end = s.j_end = -1; s.flags = 0; s.i0 = s.j0 = 0; s.box_cls = 0;
-  s.box_n = 0; s.code_off = 0; s.box_m = 0; s.pad = 0;
-  A.st[k] = s;
-  if (p.a_len == 0 || p.b_len == 0) return;
+  const unsigned lane = threadIdx.x & 31;
+  const bool in = k < A.n_pairs;
+  sw_pair_t p;
+  p.a_len = 0;
+  p.b_len = 0;
+  if (in) {
+    p = A.pairs[k];
+    PairState s;
+    s.best = 0; s.i_end = s.j_end = -1; s.flags = 0; s.i0 = s.j0 = 0; s.box_cls = 0;
+    s.box_n = 0; s.code_off = 0; s.box_m = 0; s.pad = 0;
+    A.st[k] = s;
+  }
+  const bool real = in && p.a_len > 0 && p.b_len > 0;
   const bool fused = allow_ckpt && (uint64_t)p.a_len * p.b_len <= kFusedMaxCells;
-  list_push(A, fused ? 6 : 0, class_of((int)p.a_len), (uint32_t)k);
-  atomicAdd(&stats[0], (unsigned long long)p.a_len * p.b_len);
-  atomicMax(&stats[1], (unsigned long long)p.b_len);
-  atomicMax(&stats[2], (unsigned long long)p.a_len);
+  const int slot = real ? (fused ? 6 : 0) * kNumClasses + class_of((int)p.a_len) : -1;
+  // one atomic per distinct list among the warp's lanes
+  const unsigned peers = __match_any_sync(0xffffffffu, slot);
+  const int leader = __ffs(peers) - 1;
+  const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+  uint32_t base = 0;
+  if (slot >= 0 && (int)lane == leader) base = atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  if (slot >= 0) A.lists[(uint64_t)slot * A.n_pairs + base + rank] = (uint32_t)k;
+  // cells and max length: warp reduction, one atomic per warp
+  unsigned long long cells = real ? (unsigned long long)p.a_len * p.b_len : 0ull;
+  unsigned long long mb = real ? p.b_len : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, mb, o);
+    mb = t > mb ? t : mb;
+  }
+  if (lane == 0) {
+    if (cells) atomicAdd(&stats[0], cells);
+    if (mb) atomicMax(&stats[1], mb);
+  }
 }
 
 // Move retry pairs back into the K3 lists.

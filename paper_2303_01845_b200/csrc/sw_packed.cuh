@@ -144,12 +144,12 @@ k_score_packed(KArgs A, int stage, int cls) {
   const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlockP + warp;
   int2 *bnd = A.bnd + gwarp * A.bnd_stride;
   const uint32_t Bs = (uint32_t)A.bias16;
-  const uint32_t BB = splat16(Bs);
-  const uint32_t OPEN2 = splat16((uint32_t)A.open_);
-  const uint32_t EXT2 = splat16((uint32_t)A.ext);
-  const uint32_t NEG2 = EXT2;                          // biased "-inf": E/F - ext == 0
-  const uint32_t HO0 = BB - OPEN2;                     // biased H - open for H == 0
-  const int32_t K2 = (A.open_ + A.prof_lo) * 0x10001;  // D = Ho_diag + u + K2
+  const uint32_t BB = A.p_bb;
+  const uint32_t OPEN2 = A.p_open2;
+  const uint32_t EXT2 = A.p_ext2;
+  const uint32_t NEG2 = A.p_ext2;                      // biased "-inf": E/F - ext == 0
+  const uint32_t HO0 = A.p_ho0;                        // biased H - open for H == 0
+  const uint32_t K2 = A.p_k2;                          // D = Ho_diag + u + K2
   const int lo = A.prof_lo;
   for (;;) {
     // two consecutive work items per warp
@@ -263,7 +263,7 @@ k_score_packed(KArgs A, int stage, int cls) {
             const uint32_t u2 = prmt(word_of(pa, r), word_of(pb, r), sel_pair(r & 3));
             L.E[r] = vmax2u(L.E[r] - EXT2, L.Ho[r]);
             F = vmax2u(F - EXT2, hoUp);
-            const uint32_t D = diag + u2 + (uint32_t)K2;
+            const uint32_t D = diag + u2 + K2;
             const uint32_t h = vmax2u(vmax2u(vmax2u(D, L.E[r]), F), BB);
             diag = L.Ho[r];
             L.Ho[r] = h - OPEN2;
