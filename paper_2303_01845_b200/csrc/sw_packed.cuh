@@ -22,6 +22,7 @@
 // checkpoints (k_tb).  Values are exact while every biased value stays below
 // 65535 - 128; a warp that gets near that re-runs both pairs in the wide path.
 #pragma once
+#include <type_traits>
 #include "sw_kernels.cuh"
 
 namespace pastis {
@@ -214,7 +215,11 @@ k_score_packed(KArgs A, int stage, int cls) {
         ringA[c & 127] = (c >= 0 && c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
         ringB[c & 127] = (c >= 0 && c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
       }
-      const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
+      const bool has_below = strip + 1 < nstrips;
+      // the per-step "row above from the previous strip" branch is compiled
+      // out of the first strip (the common, single-strip case)
+      auto run_strip = [&](auto above_tag) {
+        constexpr bool has_above = decltype(above_tag)::value;
       BoundaryReader br;
       const int2 dflt = make_int2((int32_t)HO0, (int32_t)NEG2);
       if (has_above) br.init(bnd, n, lane, dflt);
@@ -260,18 +265,23 @@ k_score_packed(KArgs A, int stage, int cls) {
           uint32_t F = upF, hoUp = upHo;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
+            // Short F chain: since open >= ext,
+            //   F[r+1] = max(F[r] - ext, H[r] - open) = max(F[r] - ext, t[r] - open)
+            // with t = max(D, E, 0) off the chain (H[r] = max(t, F[r])).
             const uint32_t u2 = prmt(word_of(pa, r), word_of(pb, r), sel_pair(r & 3));
             L.E[r] = vmax2u(L.E[r] - EXT2, L.Ho[r]);
-            F = vmax2u(F - EXT2, hoUp);
             const uint32_t D = diag + u2 + K2;
-            const uint32_t h = vmax2u(vmax2u(vmax2u(D, L.E[r]), F), BB);
+            const uint32_t t = vmax2u(vmax2u(D, L.E[r]), BB);
+            F = vmax2u(F - EXT2, hoUp);
+            const uint32_t h = vmax2u(t, F);
             diag = L.Ho[r];
             L.Ho[r] = h - OPEN2;
-            hoUp = L.Ho[r];
+            hoUp = t - OPEN2;
             L.rm[r] = vmax2u(L.rm[r], h);
           }
-          L.botHo = hoUp;
+          L.botHo = L.Ho[R - 1];
           L.botF = F;
+          hoUp = L.botHo;
           if (has_below && lane == 31 && c >= 0 && c < n) bnd[c] = make_int2((int32_t)hoUp, (int32_t)F);
           stageA[bslot + q] = prmt(hoUp, F, 0x5410u);
           stageB[bslot + q] = prmt(hoUp, F, 0x7632u);
@@ -304,6 +314,9 @@ k_score_packed(KArgs A, int stage, int cls) {
           }
         }
       }
+      };
+      if (strip > 0) run_strip(std::true_type{});
+      else run_strip(std::false_type{});
       // strip reduction: best and the first row reaching it, per pair
 #pragma unroll
       for (int r = 0; r < R; ++r) {
