@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=3000,
                     help="pairs in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default=WORKLOAD, choices=["config2", "config3", "config5"],
+                    help="exploration only; the headline bench is config2")
     return ap.parse_args()
 
 
@@ -196,7 +198,12 @@ def main():
 
     lib = _native.load()
     params = _native.make_params(GAP[0], GAP[1], blosum62.MATRIX)
-    sa, sb = workloads.config2(args.pairs, seed=2303 + rank, length=LENGTH)
+    if args.workload == "config2":
+        sa, sb = workloads.config2(args.pairs, seed=2303 + rank, length=LENGTH)
+    elif args.workload == "config3":
+        sa, sb = workloads.config3(args.pairs, seed=2303 + rank)
+    else:
+        sa, sb = workloads.config5(args.pairs, seed=2303 + rank)
     arena_np, table_np = pack_codes(sa, sb)
     cells = int(np.dot(table_np["a_len"].astype(np.int64), table_np["b_len"].astype(np.int64)))
     n_pairs = len(table_np)
@@ -299,10 +306,14 @@ def main():
     # integer/DPX roofline of the forward kernel (K1), measured DPX issue rate
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     csum = clocks.summary()
-    dpx_lane_ops_per_clk_sm = 64.0   # tools/microbench/dpx_rate.cu on B200 (profiles/)
-    dpx_ops_per_cell = 4.0           # E, F, H(vimax3), argmax key
+    # Integer issue roofline of the minimal Gotoh cell in packed u16x2 form
+    # (two cells per lane-op): 4 adds + 5 maxes = 9 issue slots per word, and
+    # no formulation needs fewer pipe cycles (measured on B200: VIMNMX full
+    # rate on the ALU pipe, IMAD half rate on the FMA pipe, DPX fused ops half
+    # rate on the ALU pipe -> profiles/r01/{dpx_rate,pipe_mix,mix2}.txt).
+    slots_per_word = 9.0
     clk_ghz = (csum.get("sm_max_mhz") or 1965.0) / 1e3
-    peak_gcups = dpx_lane_ops_per_clk_sm * sms * clk_ghz / dpx_ops_per_cell
+    peak_gcups = sms * clk_ghz * 4 * 32 * 2 / slots_per_word
     fwd_gcups = cells * args.steps / (float(np.sum(fwd_ms)) / 1e3) / 1e9
     line = {
         "metric": METRIC,
@@ -322,17 +333,19 @@ def main():
         "phase_ms_per_step": {"forward": float(np.mean(fwd_ms)), "reverse": float(np.mean(rev_ms)),
                               "traceback": float(np.mean(tb_ms))},
         "results_ok": ok,
-        "config": {"workload": f"{WORKLOAD}: {args.pairs} pairs/GPU of {LENGTH}x{LENGTH}, "
-                               f"BLOSUM62, gap {GAP[0]}/{GAP[1]}, 50% homologs",
+        "config": {"workload": (f"{WORKLOAD}: {args.pairs} pairs/GPU of {LENGTH}x{LENGTH}, "
+                                f"BLOSUM62, gap {GAP[0]}/{GAP[1]}, 50% homologs")
+                   if args.workload == "config2" else
+                   f"{args.workload}: {args.pairs} pairs/GPU, BLOSUM62, gap {GAP[0]}/{GAP[1]}",
                    "pairs_per_gpu": args.pairs, "cells_per_gpu_per_step": cells,
                    "l2": "flushed between timed steps (256 MiB memset, outside the events)",
                    "parallelism": f"weak-scaled shards x{world}"},
-        "roofline": {"bound": "int-dpx", "kernel": "k_score<R=10,FWD> (K1 forward)",
+        "roofline": {"bound": "int-issue", "kernel": "k_score_packed<R=10> (K1 forward, 2 pairs/warp)",
                      "achieved": fwd_gcups, "peak": peak_gcups, "unit": "GCUPS",
                      "frac": fwd_gcups / peak_gcups,
-                     "peak_basis": f"{dpx_lane_ops_per_clk_sm:.0f} DPX lane-ops/clk/SM (measured, "
-                                   f"tools/microbench) x {sms} SMs x {clk_ghz:.3f} GHz / "
-                                   f"{dpx_ops_per_cell:.0f} DPX ops per cell",
+                     "peak_basis": f"{sms} SMs x {clk_ghz:.3f} GHz x 4 SMSP x 32 lanes x 2 cells "
+                                   f"(u16x2) / {slots_per_word:.0f} issue slots per packed Gotoh "
+                                   "cell (4 adds + 5 maxes); pipe rates measured in tools/microbench",
                      "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 32/(m*n) = 0.0070 B "
                                  "-> non-binding (HBM would allow ~9e14 CUPS)",
                      "traffic": None},

@@ -21,6 +21,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "sw_kernels.cuh"
 #include "sw_packed.cuh"
 
@@ -78,7 +80,12 @@ struct DeviceCtx {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   DevBuf arena, codes, pairs, out, st, lists, ctrs, stats, mat, lut, bnd, pool;
+  DevBuf skeys, svals, cubtmp;  // work-list sort
   cudaEvent_t ev[16];
+  // one stream per length class: the packed forward + tile traceback of each
+  // class run concurrently so the tail of one class overlaps the others
+  cudaStream_t cstream[kNumClasses];
+  cudaEvent_t ev_fork, ev_k1[kNumClasses], ev_tb[kNumClasses];
   KernelInfo fwd[kNumClasses], rev[kNumClasses], box[kNumClasses], ckpt[kNumClasses];
   KernelInfo tb[kNumClasses];
   KernelInfo fwd_wide, rev_wide;
@@ -162,6 +169,12 @@ int get_ctx(int device, DeviceCtx **out) {
     CU(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto &e : c->ev) CU(cudaEventCreate(&e));
+    CU(cudaEventCreate(&c->ev_fork));
+    for (int k = 0; k < kNumClasses; ++k) {
+      CU(cudaStreamCreateWithFlags(&c->cstream[k], cudaStreamNonBlocking));
+      CU(cudaEventCreate(&c->ev_k1[k]));
+      CU(cudaEventCreateWithFlags(&c->ev_tb[k], cudaEventDisableTiming));
+    }
     int rc = setup_classes<0>(c);
     if (rc) return rc;
     rc = setup_kernel(k_score<16, 0, true>, c->sms, c->fwd_wide, c->max_warps);
@@ -277,8 +290,27 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
       const char *e = getenv("PASTIS_SW_TRACEBACK");
       return (e && strcmp(e, "box") == 0) ? 0 : 1;
     }();
-    k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(A, (unsigned long long *)c->stats.p,
-                                                                env_ckpt && packed_ok);
+    CU(c->skeys.ensure(2 * n_pairs * sizeof(unsigned long long)));
+    CU(c->svals.ensure(2 * n_pairs * sizeof(uint32_t)));
+    unsigned long long *k_in = (unsigned long long *)c->skeys.p, *k_out = k_in + n_pairs;
+    uint32_t *v_in = (uint32_t *)c->svals.p, *v_out = v_in + n_pairs;
+    static const int sort_cells = [] {
+      const char *e = getenv("PASTIS_SW_SORT");
+      return (e && strcmp(e, "shape") == 0) ? 0 : 1;
+    }();
+    k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
+        A, (unsigned long long *)c->stats.p, env_ckpt && packed_ok, k_in, v_in, sort_cells);
+    ++launches;
+    CU(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out,
+                                       (int)n_pairs, 0, 55, s));
+    CU(c->cubtmp.ensure(tmp_bytes));
+    CU(cub::DeviceRadixSort::SortPairs(c->cubtmp.p, tmp_bytes, k_in, k_out, v_in, v_out,
+                                       (int)n_pairs, 0, 55, s));
+    launches += 4;
+    k_scatter_lists<<<(unsigned)std::min<uint64_t>((n_pairs + 255) / 256, (uint64_t)c->sms * 8), 256,
+                      0, s>>>(A, k_out, v_out);
     ++launches;
     CU(cudaGetLastError());
   }
@@ -304,10 +336,21 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   const double h2 = now_ms();
 
   CU(cudaEventRecord(c->ev[1], s));
-  for (int cls = 0; cls < kNumClasses; ++cls) {  // short/medium pairs: packed forward + checkpoints
-    c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, s>>>(A, 6, cls);
-    ++launches;
+  // short/medium pairs: packed forward + checkpoints, then the tile traceback,
+  // one stream per length class
+  CU(cudaEventRecord(c->ev_fork, s));
+  for (int cls = 0; cls < kNumClasses; ++cls) {
+    cudaStream_t cs = c->cstream[cls];
+    CU(cudaStreamWaitEvent(cs, c->ev_fork, 0));
+    c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, cs>>>(A, 6, cls);
+    CU(cudaEventRecord(c->ev_k1[cls], cs));
+    c->tb[cls].fn<<<c->tb[cls].grid, kTbWarps * 32, 0, cs>>>(A, 7, cls);
+    CU(cudaEventRecord(c->ev_tb[cls], cs));
+    launches += 2;
   }
+  // the scalar path below also takes the packed pass's fallbacks
+  for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_k1[cls], 0));
+  CU(cudaEventRecord(c->ev[6], s));   // start of the scalar (long-pair) forward
   for (int cls = 0; cls < kNumClasses; ++cls) {  // long pairs: score-only forward
     c->fwd[cls].fn<<<c->fwd[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 0, cls);
     ++launches;
@@ -324,10 +367,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   ++launches;
   CU(cudaGetLastError());
   CU(cudaEventRecord(c->ev[3], s));
-  for (int cls = 0; cls < kNumClasses; ++cls) {  // tile traceback from the checkpoints
-    c->tb[cls].fn<<<c->tb[cls].grid, kTbWarps * 32, 0, s>>>(A, 7, cls);
-    ++launches;
-  }
+  for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_tb[cls], 0));
   double tb_ms = 0.0;
   for (int round = 0;; ++round) {
     for (int cls = 0; cls < kNumClasses; ++cls) {
@@ -356,7 +396,12 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 5 * kNumClasses, 0, 4, s));
   }
   if (tm) {
-    tm->forward_ms += ev_ms(c->ev[1], c->ev[2]);
+    // forward = packed forward of the short/medium classes (concurrent
+    // streams: the latest one to finish) + the scalar forward of long pairs
+    double fwd_packed = 0.0;
+    for (int cls = 0; cls < kNumClasses; ++cls)
+      fwd_packed = std::max(fwd_packed, (double)ev_ms(c->ev_fork, c->ev_k1[cls]));
+    tm->forward_ms += fwd_packed + ev_ms(c->ev[6], c->ev[2]);
     tm->reverse_ms += ev_ms(c->ev[2], c->ev[3]);
     tm->traceback_ms += tb_ms;
     tm->kernel_ms += ev_ms(c->ev[0], c->ev[1]) + ev_ms(c->ev[1], c->ev[3]) + tb_ms;
@@ -562,7 +607,7 @@ void sw_release(int device) {
     std::lock_guard<std::mutex> g2(c->mu);
     cudaSetDevice((int)d);
     for (DevBuf *b : {&c->arena, &c->codes, &c->pairs, &c->out, &c->st, &c->lists, &c->ctrs,
-                      &c->stats, &c->bnd, &c->pool})
+                      &c->stats, &c->bnd, &c->pool, &c->skeys, &c->svals, &c->cubtmp})
       b->release();
   }
 }

@@ -42,18 +42,27 @@ constexpr int kProfBytes = kCodes * kProfStride;  // 13,312 B per warp
 constexpr int kMatBytes = 688;           // 26*26 int8, padded to 16
 constexpr int kStageBytes = 16 * 8 * 4;  // per-warp row-checkpoint staging (16 boundaries x 8 steps)
 constexpr int kWarpsPerBlock = 4;
-constexpr int kNumClasses = 5;
+constexpr int kNumClasses = 6;
 constexpr int kStages = 8;  // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
                             // 6 K1 with checkpoints, 7 tile traceback
 constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take the fused path
 constexpr int32_t kScaledLimit = 32767 - 128;
 constexpr int32_t kNegInf = -(1 << 30);
 
+// Length classes: R rows per lane, 32R rows per strip.  A pair with m rows
+// takes the class whose strips pad m the least (ties: larger R, fewer strips).
 __host__ __device__ constexpr int class_rows(int cls) {
-  return cls == 0 ? 4 : cls == 1 ? 8 : cls == 2 ? 10 : cls == 3 ? 12 : 16;
+  return cls == 0 ? 4 : cls == 1 ? 6 : cls == 2 ? 8 : cls == 3 ? 10 : cls == 4 ? 12 : 16;
 }
 __host__ __device__ inline int class_of(int m) {
-  return m <= 128 ? 0 : m <= 256 ? 1 : m <= 320 ? 2 : m <= 384 ? 3 : 4;
+  int best = kNumClasses - 1;
+  long best_rows = 1L << 40;
+  for (int c = kNumClasses - 1; c >= 0; --c) {
+    const long rows_per_strip = 32L * class_rows(c);
+    const long rows = (m + rows_per_strip - 1) / rows_per_strip * rows_per_strip;
+    if (rows < best_rows) { best_rows = rows; best = c; }
+  }
+  return best;
 }
 __host__ __device__ constexpr int box_lane_bytes(int R) { return R <= 4 ? 2 : R <= 8 ? 4 : 8; }
 
@@ -1108,9 +1117,15 @@ __global__ void k_encode(const uint8_t *__restrict__ raw, uint8_t *__restrict__ 
     codes[i] = slut[raw[i]];
 }
 
-// Classify pairs by row count into work lists (warp-aggregated appends);
-// count cells; reset per-pair state.
-__global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt) {
+// Classify pairs by row count (work list = stage x length class), count the
+// lists (warp-aggregated atomics) and emit a sort key per pair:
+// (list << 48) | (65535 - m) << 16 | (65535 - n).  A radix sort then orders
+// every list by descending shape (largest first; neighbours of the same shape
+// for the packed kernel, which aligns two consecutive pairs per warp) and
+// k_scatter_lists writes the sorted lists.
+constexpr int kNoList = 127;
+__global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt,
+                           unsigned long long *keys, uint32_t *vals, int sort_cells) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
   const bool in = k < A.n_pairs;
@@ -1125,28 +1140,51 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt) {
     A.st[k] = s;
   }
   const bool real = in && p.a_len > 0 && p.b_len > 0;
-  const bool fused = allow_ckpt && (uint64_t)p.a_len * p.b_len <= kFusedMaxCells;
+  const uint64_t cells = (uint64_t)p.a_len * p.b_len;
+  const bool fused = allow_ckpt && cells <= kFusedMaxCells;
   const int slot = real ? (fused ? 6 : 0) * kNumClasses + class_of((int)p.a_len) : -1;
-  // one atomic per distinct list among the warp's lanes
   const unsigned peers = __match_any_sync(0xffffffffu, slot);
   const int leader = __ffs(peers) - 1;
-  const unsigned rank = __popc(peers & ((1u << lane) - 1u));
-  uint32_t base = 0;
-  if (slot >= 0 && (int)lane == leader) base = atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));
-  base = __shfl_sync(peers, base, leader);
-  if (slot >= 0) A.lists[(uint64_t)slot * A.n_pairs + base + rank] = (uint32_t)k;
-  // cells and max length: warp reduction, one atomic per warp
-  unsigned long long cells = real ? (unsigned long long)p.a_len * p.b_len : 0ull;
+  if (slot >= 0 && (int)lane == leader) atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));
+  if (in) {
+    const unsigned long long order =
+        sort_cells ? ((0xFFFFFFFFFFFFull - cells) & 0xFFFFFFFFFFFFull)
+                   : (((unsigned long long)(0xFFFFu - min(p.a_len, 0xFFFFu)) << 16) |
+                      (unsigned long long)(0xFFFFu - min(p.b_len, 0xFFFFu)));
+    keys[k] = ((unsigned long long)(slot >= 0 ? slot : kNoList) << 48) | order;
+    vals[k] = (uint32_t)k;
+  }
+  unsigned long long c = real ? cells : 0ull;
   unsigned long long mb = real ? p.b_len : 0ull;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
     const unsigned long long t = __shfl_xor_sync(0xffffffffu, mb, o);
     mb = t > mb ? t : mb;
   }
   if (lane == 0) {
-    if (cells) atomicAdd(&stats[0], cells);
+    if (c) atomicAdd(&stats[0], c);
     if (mb) atomicMax(&stats[1], mb);
+  }
+}
+
+// Sorted (key, pair) -> per-list arrays; list offsets are the exclusive
+// prefix of the list counts in key order (lists are contiguous in the sort).
+__global__ void k_scatter_lists(KArgs A, const unsigned long long *keys, const uint32_t *vals) {
+  __shared__ uint32_t off[kStages * kNumClasses];
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int i = 0; i < kStages * kNumClasses; ++i) {
+      off[i] = acc;
+      acc += A.ctrs[i];
+    }
+  }
+  __syncthreads();
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < A.n_pairs;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const int slot = (int)(keys[p] >> 48);
+    if (slot >= kStages * kNumClasses) continue;
+    A.lists[(uint64_t)slot * A.n_pairs + (p - off[slot])] = vals[p];
   }
 }
 

@@ -115,6 +115,36 @@ __device__ __forceinline__ uint32_t sel_pair(int k) {
          ((uint32_t)((4 + k) | 8) << 12);
 }
 
+// The previous strip's bottom row comes from the row checkpoints of its
+// lane 31 (boundary nb-1), indexed by that lane's step = column + 31; both
+// pairs' words are fetched 32 columns ahead and repacked into u16x2.
+struct PackedBoundaryReader {
+  uint32_t a_cur, b_cur, a_nxt, b_nxt;
+  const uint32_t *ra, *rb;    // row-checkpoint rows (nullptr: pair without checkpoints)
+  int n;
+  __device__ __forceinline__ uint32_t ld(const uint32_t *r, int c, uint32_t dflt) const {
+    return (r && c < n) ? r[c + 31] : dflt;
+  }
+  __device__ __forceinline__ void init(const uint32_t *ra_, const uint32_t *rb_, int n_, int lane,
+                                       uint32_t dflt) {
+    ra = ra_; rb = rb_; n = n_;
+    a_cur = ld(ra, lane, dflt); b_cur = ld(rb, lane, dflt);
+    a_nxt = ld(ra, 32 + lane, dflt); b_nxt = ld(rb, 32 + lane, dflt);
+  }
+  // (Ho2, F2) for column s (lane 0's column), all lanes participate
+  __device__ __forceinline__ void get(int s, int lane, uint32_t dflt, uint32_t &ho2, uint32_t &f2) {
+    if ((s & 31) == 0 && s > 0) {
+      a_cur = a_nxt; b_cur = b_nxt;
+      a_nxt = ld(ra, s + 32 + lane, dflt);
+      b_nxt = ld(rb, s + 32 + lane, dflt);
+    }
+    const uint32_t wa = __shfl_sync(0xffffffffu, a_cur, s & 31);
+    const uint32_t wb = __shfl_sync(0xffffffffu, b_cur, s & 31);
+    ho2 = prmt(wa, wb, 0x5410u);
+    f2 = prmt(wa, wb, 0x7632u);
+  }
+};
+
 template <int R>
 struct PackedLane {
   uint32_t Ho[R], E[R], rm[R];
@@ -142,8 +172,6 @@ k_score_packed(KArgs A, int stage, int cls) {
   uint8_t *ringA = reinterpret_cast<uint8_t *>(stageB + 17 * 8);
   uint8_t *ringB = ringA + 128;
   load_matrix(smat, A.mat);
-  const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlockP + warp;
-  int2 *bnd = A.bnd + gwarp * A.bnd_stride;
   const uint32_t Bs = (uint32_t)A.bias16;
   const uint32_t BB = A.p_bb;
   const uint32_t OPEN2 = A.p_open2;
@@ -215,14 +243,18 @@ k_score_packed(KArgs A, int stage, int cls) {
         ringA[c & 127] = (c >= 0 && c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
         ringB[c & 127] = (c >= 0 && c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
       }
-      const bool has_below = strip + 1 < nstrips;
       // the per-step "row above from the previous strip" branch is compiled
       // out of the first strip (the common, single-strip case)
       auto run_strip = [&](auto above_tag) {
         constexpr bool has_above = decltype(above_tag)::value;
-      BoundaryReader br;
-      const int2 dflt = make_int2((int32_t)HO0, (int32_t)NEG2);
-      if (has_above) br.init(bnd, n, lane, dflt);
+      PackedBoundaryReader br;
+      const uint32_t dflt = (HO0 & 0xFFFFu) | (NEG2 << 16);   // (H-open at H=0, F=-inf)
+      if (has_above) {
+        const uint64_t prev = (uint64_t)(strip - 1) * CL.strip_words + CL.col_words +
+                              (uint64_t)(CL.nb - 1) * CL.spad;
+        br.init(P[0].ck ? P[0].ck + prev : nullptr, P[1].ck ? P[1].ck + prev : nullptr, n, lane,
+                dflt);
+      }
       // checkpoint destinations for this strip
       uint32_t *colA = P[0].ck ? P[0].ck + (uint64_t)strip * CL.strip_words + lane : nullptr;
       uint32_t *colB = P[1].ck ? P[1].ck + (uint64_t)strip * CL.strip_words + lane : nullptr;
@@ -255,8 +287,9 @@ k_score_packed(KArgs A, int stage, int cls) {
           uint32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
           uint32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
           if (has_above) {
-            const int2 bv = br.get(bnd, s, n, lane, dflt);
-            if (lane == 0) { upHo = (uint32_t)bv.x; upF = (uint32_t)bv.y; }
+            uint32_t bho, bf;
+            br.get(s, lane, dflt, bho, bf);
+            if (lane == 0) { upHo = bho; upF = bf; }
           } else if (lane == 0) {
             upHo = HO0; upF = NEG2;
           }
@@ -282,7 +315,6 @@ k_score_packed(KArgs A, int stage, int cls) {
           L.botHo = L.Ho[R - 1];
           L.botF = F;
           hoUp = L.botHo;
-          if (has_below && lane == 31 && c >= 0 && c < n) bnd[c] = make_int2((int32_t)hoUp, (int32_t)F);
           stageA[bslot + q] = prmt(hoUp, F, 0x5410u);
           stageB[bslot + q] = prmt(hoUp, F, 0x7632u);
         }
