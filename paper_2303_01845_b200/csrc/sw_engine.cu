@@ -294,9 +294,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(c->svals.ensure(2 * n_pairs * sizeof(uint32_t)));
     unsigned long long *k_in = (unsigned long long *)c->skeys.p, *k_out = k_in + n_pairs;
     uint32_t *v_in = (uint32_t *)c->svals.p, *v_out = v_in + n_pairs;
+    // work lists sorted by shape (m, n descending) by default;
+    // PASTIS_SW_SORT=cells sorts by cell count instead (A/B comparisons)
     static const int sort_cells = [] {
       const char *e = getenv("PASTIS_SW_SORT");
-      return (e && strcmp(e, "shape") == 0) ? 0 : 1;
+      return (e && strcmp(e, "cells") == 0) ? 1 : 0;
     }();
     k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
         A, (unsigned long long *)c->stats.p, env_ckpt && packed_ok, k_in, v_in, sort_cells);
@@ -348,21 +350,24 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(cudaEventRecord(c->ev_tb[cls], cs));
     launches += 2;
   }
-  // the scalar path below also takes the packed pass's fallbacks
+  // long pairs: scalar forward (one class) concurrently with the packed classes
+  c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
+      A, 0, kLongClass);
+  ++launches;
+  CU(cudaEventRecord(c->ev[7], s));   // end of the concurrent scalar forward
+  // then the packed pass's fallbacks (same list, the cursor resumes)
   for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_k1[cls], 0));
-  CU(cudaEventRecord(c->ev[6], s));   // start of the scalar (long-pair) forward
-  for (int cls = 0; cls < kNumClasses; ++cls) {  // long pairs: score-only forward
-    c->fwd[cls].fn<<<c->fwd[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 0, cls);
-    ++launches;
-  }
+  CU(cudaEventRecord(c->ev[6], s));   // start of the scalar (long-pair) tail
+  c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
+      A, 0, kLongClass);
+  ++launches;
   c->fwd_wide.fn<<<c->fwd_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 3, 0);
   ++launches;
   CU(cudaGetLastError());
   CU(cudaEventRecord(c->ev[2], s));
-  for (int cls = 0; cls < kNumClasses; ++cls) {
-    c->rev[cls].fn<<<c->rev[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 1, cls);
-    ++launches;
-  }
+  c->rev[kLongClass].fn<<<c->rev[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
+      A, 1, kLongClass);
+  ++launches;
   c->rev_wide.fn<<<c->rev_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 4, 0);
   ++launches;
   CU(cudaGetLastError());
@@ -396,12 +401,13 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 5 * kNumClasses, 0, 4, s));
   }
   if (tm) {
-    // forward = packed forward of the short/medium classes (concurrent
-    // streams: the latest one to finish) + the scalar forward of long pairs
-    double fwd_packed = 0.0;
+    // forward = the forward passes that run concurrently after the fork: the
+    // packed classes (their own streams) and the scalar long-pair pass (main
+    // stream); the rare fallback re-run is not included (it is in kernel_ms)
+    double fwd = ev_ms(c->ev_fork, c->ev[7]);
     for (int cls = 0; cls < kNumClasses; ++cls)
-      fwd_packed = std::max(fwd_packed, (double)ev_ms(c->ev_fork, c->ev_k1[cls]));
-    tm->forward_ms += fwd_packed + ev_ms(c->ev[6], c->ev[2]);
+      fwd = std::max(fwd, (double)ev_ms(c->ev_fork, c->ev_k1[cls]));
+    tm->forward_ms += fwd;
     tm->reverse_ms += ev_ms(c->ev[2], c->ev[3]);
     tm->traceback_ms += tb_ms;
     tm->kernel_ms += ev_ms(c->ev[0], c->ev[1]) + ev_ms(c->ev[1], c->ev[3]) + tb_ms;

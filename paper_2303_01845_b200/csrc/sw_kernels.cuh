@@ -43,6 +43,7 @@ constexpr int kMatBytes = 688;           // 26*26 int8, padded to 16
 constexpr int kStageBytes = 16 * 8 * 4;  // per-warp row-checkpoint staging (16 boundaries x 8 steps)
 constexpr int kWarpsPerBlock = 4;
 constexpr int kNumClasses = 6;
+constexpr int kLongClass = kNumClasses - 1;  // R = 16: the only class of the long-pair path
 constexpr int kStages = 8;  // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
                             // 6 K1 with checkpoints, 7 tile traceback
 constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take the fused path
@@ -268,16 +269,19 @@ __device__ __forceinline__ void score_step(ScoreLane<R, WIDE> &L, const uint8_t 
   int32_t F = upF, hoUp = upHo;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
+    // short F chain (open >= ext): F[r+1] = max(F[r] - ext, max(D, E, 0) - open),
+    // see sw_packed.cuh; H = max(t, F) stays off the chain
     const uint32_t w = word_of(pw, r);
     const int32_t sc = (int32_t)prmt(w, 0u, WIDE ? sel_plain(r & 3) : sel_scaled(r & 3));
     L.E[r] = __viaddmax_s32(L.E[r], nEXT, L.Ho[r]);
-    F = __viaddmax_s32(F, nEXT, hoUp);
     const int32_t D = diag + sc + OPEN;
-    const int32_t h = __vimax3_s32_relu(D, L.E[r], F);
+    const int32_t t = __vimax_s32_relu(D, L.E[r]);
+    F = __viaddmax_s32(F, nEXT, hoUp);
+    const int32_t h = max(t, F);
     diag = L.Ho[r];
     const int32_t ho = h - OPEN;
     L.Ho[r] = ho;
-    hoUp = ho;
+    hoUp = t - OPEN;
     if constexpr (WIDE) {
       const long long kk = ((long long)h << 32) | (uint32_t)cc;
       L.key[r] = kk > L.key[r] ? kk : L.key[r];
@@ -285,7 +289,7 @@ __device__ __forceinline__ void score_step(ScoreLane<R, WIDE> &L, const uint8_t 
       L.key[r] = __viaddmax_s32(ho, cc + OPEN, L.key[r]);
     }
   }
-  L.botHo = hoUp;
+  L.botHo = L.Ho[R - 1];
   L.botF = F;
   if (has_below && lane == 31 && valid) bnd[c] = make_int2(L.botHo, L.botF);
 }
@@ -340,7 +344,7 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
       ck_nwin = CL.nwin;
     }
     for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
-#pragma unroll
+#pragma unroll 2
       for (int q = 0; q < kScoreUnroll; ++q) {
         score_step<R, MODE, WIDE>(L, prof, cols, s0 + q, n, lane, has_above, has_below, br, bnd,
                                   dflt, OPEN, nEXT);
@@ -474,7 +478,7 @@ k_score(KArgs A, int stage, int cls) {
               st->j0 = 0;
               list_push(A, 2, class_of(i_end + 1), (uint32_t)k);
             } else {
-              list_push(A, 1, class_of(i_end + 1), (uint32_t)k);
+              list_push(A, 1, kLongClass, (uint32_t)k);
             }
           }
         }
@@ -1142,7 +1146,9 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt,
   const bool real = in && p.a_len > 0 && p.b_len > 0;
   const uint64_t cells = (uint64_t)p.a_len * p.b_len;
   const bool fused = allow_ckpt && cells <= kFusedMaxCells;
-  const int slot = real ? (fused ? 6 : 0) * kNumClasses + class_of((int)p.a_len) : -1;
+  // short/medium pairs: packed pass, per length class; long pairs: one
+  // scalar class (R = 16), so each long-pair phase has a single tail
+  const int slot = real ? (fused ? 6 * kNumClasses + class_of((int)p.a_len) : kLongClass) : -1;
   const unsigned peers = __match_any_sync(0xffffffffu, slot);
   const int leader = __ffs(peers) - 1;
   if (slot >= 0 && (int)lane == leader) atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));
