@@ -25,6 +25,7 @@
 
 #include "sw_kernels.cuh"
 #include "sw_packed.cuh"
+#include "sw_cta.cuh"
 
 using namespace pastis;
 
@@ -88,7 +89,7 @@ struct DeviceCtx {
   cudaEvent_t ev_fork, ev_k1[kNumClasses], ev_tb[kNumClasses];
   KernelInfo fwd[kNumClasses], rev[kNumClasses], box[kNumClasses], ckpt[kNumClasses];
   KernelInfo tb[kNumClasses];
-  KernelInfo fwd_wide, rev_wide;
+  KernelInfo fwd_wide, rev_wide, fwd_cta, rev_cta;
   int max_warps = 0;
   bool ready = false;
 };
@@ -121,6 +122,18 @@ int setup_packed(K fn, int sms, int smem, KernelInfo &ki, int &max_warps) {
   ki.grid = nb * sms;
   ki.smem = smem;
   max_warps = std::max(max_warps, ki.grid * kWarpsPerBlockP);
+  return SW_OK;
+}
+
+template <typename K>
+int setup_cta(K fn, int sms, KernelInfo &ki) {
+  CU(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCta));
+  int nb = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)fn, kCtaWarps * 32, kSmemCta));
+  if (nb < 1) return fail(SW_ECUDA, "CTA kernel cannot be resident");
+  ki.fn = (KernelFn)fn;
+  ki.grid = nb * sms;
+  ki.smem = kSmemCta;
   return SW_OK;
 }
 
@@ -180,6 +193,10 @@ int get_ctx(int device, DeviceCtx **out) {
     rc = setup_kernel(k_score<16, 0, true>, c->sms, c->fwd_wide, c->max_warps);
     if (rc) return rc;
     rc = setup_kernel(k_score<16, 1, true>, c->sms, c->rev_wide, c->max_warps);
+    if (rc) return rc;
+    rc = setup_cta(k_score_cta<kCtaRowsR, 0>, c->sms, c->fwd_cta);
+    if (rc) return rc;
+    rc = setup_cta(k_score_cta<kCtaRowsR, 1>, c->sms, c->rev_cta);
     if (rc) return rc;
     // LUT (align.py:27-30) and matrix buffers
     CU(c->lut.ensure(256));
@@ -350,10 +367,12 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(cudaEventRecord(c->ev_tb[cls], cs));
     launches += 2;
   }
-  // long pairs: scalar forward (one class) concurrently with the packed classes
+  // long pairs: scalar forward concurrently with the packed classes -- one CTA
+  // per pair for pairs of >= 4 strips, one warp per pair for the others
+  c->fwd_cta.fn<<<c->fwd_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 0, kCtaClass);
   c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
       A, 0, kLongClass);
-  ++launches;
+  launches += 2;
   CU(cudaEventRecord(c->ev[7], s));   // end of the concurrent scalar forward
   // then the packed pass's fallbacks (same list, the cursor resumes)
   for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_k1[cls], 0));
@@ -365,9 +384,10 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   ++launches;
   CU(cudaGetLastError());
   CU(cudaEventRecord(c->ev[2], s));
+  c->rev_cta.fn<<<c->rev_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 1, kCtaClass);
   c->rev[kLongClass].fn<<<c->rev[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
       A, 1, kLongClass);
-  ++launches;
+  launches += 2;
   c->rev_wide.fn<<<c->rev_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 4, 0);
   ++launches;
   CU(cudaGetLastError());

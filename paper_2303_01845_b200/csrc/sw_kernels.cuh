@@ -44,6 +44,12 @@ constexpr int kStageBytes = 16 * 8 * 4;  // per-warp row-checkpoint staging (16 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kNumClasses = 6;
 constexpr int kLongClass = kNumClasses - 1;  // R = 16: the only class of the long-pair path
+constexpr int kCtaClass = 0;    // long pairs with >= 4 strips: one CTA per pair (sw_cta.cuh)
+constexpr int kCtaRowsR = 16;   // rows per lane of the CTA kernels
+constexpr int kCtaStripsMin = 4;
+__host__ __device__ inline int long_class(int m) {
+  return (m + 32 * kCtaRowsR - 1) / (32 * kCtaRowsR) >= kCtaStripsMin ? kCtaClass : kLongClass;
+}
 constexpr int kStages = 8;  // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
                             // 6 K1 with checkpoints, 7 tile traceback
 constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take the fused path
@@ -478,7 +484,7 @@ k_score(KArgs A, int stage, int cls) {
               st->j0 = 0;
               list_push(A, 2, class_of(i_end + 1), (uint32_t)k);
             } else {
-              list_push(A, 1, kLongClass, (uint32_t)k);
+              list_push(A, 1, long_class(i_end + 1), (uint32_t)k);
             }
           }
         }
@@ -817,7 +823,9 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
     T.H[q + 1][x0] = (int16_t)(Ho + OPEN);
     if (rq == 0) T.H[q][x0] = (int16_t)(hoUpPrevT + OPEN);
   }
-  // top halo row: H of the row above the tile at columns c_lo(t0) .. +31
+  // top halo row: H of the row above the tile at columns c_lo(t0) .. +31;
+  // lane l also keeps (Ho, F) of column c_lo(t0) + l packed for row 0's feed
+  uint32_t topv;
   {
     int32_t tHo = -OPEN, tF = kNeg16;
     const uint32_t *toprow = nullptr;
@@ -838,27 +846,57 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
       }
     }
     T.H[0][t1 - t0 + 1 + lane] = (int16_t)(tHo + OPEN);
-    T.F[0][t1 - t0 + 1 + lane] = (int16_t)tF;
+    topv = ((uint32_t)tHo & 0xFFFFu) | ((uint32_t)tF << 16);
   }
-  int32_t outHo = Ho, outF = (rq == R - 1) ? FbotT : (int32_t)kNeg16;
+  // The walk leaves this tile to the left (window w-1) or upwards (group
+  // g-1): prefetch those tiles' checkpoint lines into L2 now, so their replay
+  // does not start with a DRAM round trip.
+  {
+    auto pf = [](const void *ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); };
+    if (w > 1 && row_ok) {
+      const uint32_t *wd = sbase + (uint64_t)(w - 1) * 32 * (2 * R + 1) + tq;
+      pf(wd + 32 * rq);
+      if (rq == 0) pf(wd + 32 * R);
+    }
+    if (t0 > 0 && w > 0) {
+      const int g2 = g - 1, t2 = g2 * CL.G;
+      const int qq = lane, tqq = t2 + qq / R, rqq = qq - (qq / R) * R;
+      if (qq < CL.G * R) {
+        const uint32_t *wd = sbase + (uint64_t)w * 32 * (2 * R + 1) + tqq;
+        pf(wd + 32 * rqq);
+        if (rqq == 0) pf(wd + 32 * R);
+      }
+      if (t2 > 0) {
+        const int idx = 32 * w - t2 + lane + (t2 - 1);
+        pf(sbase + CL.col_words + (uint64_t)ck_boundary(t2 - 1, CL) * CL.spad + idx);
+      }
+    }
+    if (w > 0 && (t0 > 0 || strip > 0)) {
+      const uint32_t *row = t0 > 0 ? sbase + CL.col_words + (uint64_t)ck_boundary(t0 - 1, CL) * CL.spad
+                                   : sbase - CL.strip_words + CL.col_words +
+                                         (uint64_t)(CL.nb - 1) * CL.spad;
+      const int idx = 32 * (w - 1) - t0 + lane + (t0 > 0 ? t0 - 1 : 31);
+      if (idx >= 0) pf(row + idx);
+    }
+  }
+  // row-to-row hand-off: (Ho, F) of the row above as one packed int16 pair
+  uint32_t out = ((uint32_t)Ho & 0xFFFFu) | ((uint32_t)((rq == R - 1) ? FbotT : (int32_t)kNeg16) << 16);
   const int32_t hoAbove = __shfl_up_sync(0xffffffffu, Ho, 1);
   int32_t prevTop = (rq == 0) ? hoUpPrevT : hoAbove;
   const int vstart = q - q / R;
   const int vlast = min(qmax - qmax / R + 31, kap_in - (32 * w - t0) + qmax);
+  const int xbase = (32 * w - t0) - q - cmin + 1;   // x = xbase + v
+  const int8_t *mrow = smat + acode * kCodes;
   __syncwarp();
+#pragma unroll 2
   for (int v = 0; v <= vlast; ++v) {
-    int32_t topHo = __shfl_up_sync(0xffffffffu, outHo, 1);
-    int32_t topF = __shfl_up_sync(0xffffffffu, outF, 1);
-    const int c = 32 * w - t0 + v - q;
-    const int x = c - cmin + 1;
-    if (q == 0) {  // row 0 reads the staged top halo
-      const int xx = min(max(x, 0), kTbX - 1);
-      topHo = (int32_t)T.H[0][xx] - OPEN;
-      topF = T.F[0][xx];
-    }
-    const bool active = row_ok & (v >= vstart) & (v <= vstart + 31);
-    if (active) {
-      const int32_t sc = smat[acode * kCodes + T.bcode[x - 1]];
+    const uint32_t up = __shfl_up_sync(0xffffffffu, out, 1);
+    const uint32_t tv = __shfl_sync(0xffffffffu, topv, v & 31);
+    const uint32_t in = q == 0 ? tv : up;
+    const int32_t topHo = (int32_t)(int16_t)(in & 0xFFFFu), topF = (int32_t)in >> 16;
+    const int x = xbase + v;
+    if (row_ok & (v >= vstart) & (v <= vstart + 31)) {
+      const int32_t sc = mrow[T.bcode[x - 1]];
       const int32_t e = max(E - EXT, Ho);
       const int32_t f = max(topF - EXT, topHo);
       const int32_t h = __vimax3_s32_relu(prevTop + sc + OPEN, e, f);
@@ -867,8 +905,7 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
       T.F[q + 1][x] = (int16_t)f;
       E = e;
       Ho = h - OPEN;
-      outHo = Ho;
-      outF = f;
+      out = ((uint32_t)Ho & 0xFFFFu) | ((uint32_t)f << 16);
       prevTop = topHo;
     }
   }
@@ -1148,7 +1185,7 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt,
   const bool fused = allow_ckpt && cells <= kFusedMaxCells;
   // short/medium pairs: packed pass, per length class; long pairs: one
   // scalar class (R = 16), so each long-pair phase has a single tail
-  const int slot = real ? (fused ? 6 * kNumClasses + class_of((int)p.a_len) : kLongClass) : -1;
+  const int slot = real ? (fused ? 6 * kNumClasses + class_of((int)p.a_len) : long_class((int)p.a_len)) : -1;
   const unsigned peers = __match_any_sync(0xffffffffu, slot);
   const int leader = __ffs(peers) - 1;
   if (slot >= 0 && (int)lane == leader) atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));
