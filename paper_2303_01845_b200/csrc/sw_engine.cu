@@ -342,8 +342,10 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   if (c->pool.bytes == 0) {
     size_t free_b = 0, total_b = 0;
     CU(cudaMemGetInfo(&free_b, &total_b));
-    const size_t cap = std::min<size_t>((size_t)(free_b * 0.5), (size_t)48 << 30);
-    CU(c->pool.ensure(std::max<size_t>(cap, (size_t)256 << 20)));
+    size_t cap = std::min<size_t>((size_t)(free_b * 0.5), (size_t)48 << 30);
+    // PASTIS_SW_POOL_MB caps the pool (exercises the overflow / retry paths)
+    if (const char *e = getenv("PASTIS_SW_POOL_MB")) cap = std::min<size_t>(cap, (size_t)atoll(e) << 20);
+    CU(c->pool.ensure(std::max<size_t>(cap, (size_t)8 << 20)));
   }
   const double h1 = now_ms();
   A.pool = (uint8_t *)c->pool.p;
@@ -374,11 +376,12 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
       A, 0, kLongClass);
   launches += 2;
   CU(cudaEventRecord(c->ev[7], s));   // end of the concurrent scalar forward
-  // then the packed pass's fallbacks (same list, the cursor resumes)
+  // then the packed pass's fallbacks (their own list, complete once every
+  // packed class has finished), on the long-pair kernel
   for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_k1[cls], 0));
   CU(cudaEventRecord(c->ev[6], s));   // start of the scalar (long-pair) tail
   c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
-      A, 0, kLongClass);
+      A, 0, kFallbackClass);
   ++launches;
   c->fwd_wide.fn<<<c->fwd_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 3, 0);
   ++launches;

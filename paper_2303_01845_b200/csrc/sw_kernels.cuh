@@ -45,6 +45,11 @@ constexpr int kWarpsPerBlock = 4;
 constexpr int kNumClasses = 6;
 constexpr int kLongClass = kNumClasses - 1;  // R = 16: the only class of the long-pair path
 constexpr int kCtaClass = 0;    // long pairs with >= 4 strips: one CTA per pair (sw_cta.cuh)
+// stage-0 list of the packed pass's no-checkpoint-room fallbacks.  Kept apart
+// from kLongClass's list: that list is drained by a launch running
+// concurrently with the packed pass, and a warp that finds a list empty still
+// advances its cursor, so items appended behind it would never be fetched.
+constexpr int kFallbackClass = 1;
 constexpr int kCtaRowsR = 16;   // rows per lane of the CTA kernels
 constexpr int kCtaStripsMin = 4;
 __host__ __device__ inline int long_class(int m) {

@@ -404,7 +404,7 @@ k_score_packed(KArgs A, int stage, int cls) {
           list_push(A, 7, cls, (uint32_t)P[h].k);
         } else {                               // no checkpoint room: scalar path
           st->flags = 0;
-          list_push(A, 0, kLongClass, (uint32_t)P[h].k);
+          list_push(A, 0, kFallbackClass, (uint32_t)P[h].k);
         }
       }
     }

@@ -196,3 +196,87 @@ def test_full_config2_properties():
     ref = oracle.align_batch_c(arena, table[pick], 11, 1, matrix("blosum62"), threads=16)
     got = np.stack([rec[f][pick] for f in FIELDS], axis=1)
     assert (got == ref[:, :7]).all()
+
+
+def test_cta_per_pair_long_vs_oracle():
+    """Pairs of >= 4 strips (2048+ rows) take the CTA-per-pair forward and
+    reverse kernels: exact against the full C oracle."""
+    rng = np.random.default_rng(17)
+    sa, sb = [], []
+    for la, lb, rel in [(2100, 2300, False), (3000, 2500, False), (4100, 1800, True),
+                        (5200, 5000, False), (2600, 6000, False), (3500, 3400, True),
+                        (2049, 2049, False), (6000, 2100, False)]:
+        a = workloads._random_seq(rng, la)
+        if rel:
+            b = workloads._fit(rng, workloads._homolog(rng, a, 0.25, 0.05), lb)
+        else:
+            b = workloads._random_seq(rng, lb)
+        sa.append(a.tobytes())
+        sb.append(b.tobytes())
+    for go, ge in [(11, 1), (11, 2)]:
+        _oracle_compare(sa, sb, go, ge)
+
+
+def test_config5_scale_properties():
+    """A config-5-size pair (20k x 25k): score and end cell against the O(n)
+    score oracle, begin/matches/length via the box lemma (re-aligning the
+    reported spans must reproduce them)."""
+    sa, sb = workloads.config5(2, seed=55, lo=20000, hi=25000)
+    arena, table = pack_codes(sa, sb)
+    mat = matrix("blosum62")
+    rec, _ = _native.align_host(arena, table, _native.make_params(11, 1, mat))
+    for k in range(len(table)):
+        a, b = sa[k], sb[k]
+        best, i_end, j_end = oracle.score_c(a, b, 11, 1, mat)
+        r = rec[k]
+        assert (int(r["score"]), int(r["i_end"]), int(r["j_end"])) == (best, i_end, j_end)
+        sub = oracle.align_c(a[r["i_begin"]:i_end + 1], b[r["j_begin"]:j_end + 1], 11, 1, mat)
+        assert sub[0] == best and sub[1] == 0 and sub[3] == 0
+        assert (sub[5], sub[6]) == (int(r["matches"]), int(r["aln_len"]))
+
+
+def test_full_config3_properties():
+    sa, sb = workloads.config3(200_000, seed=2304)
+    arena, table = pack_codes(sa, sb)
+    p = _native.make_params(11, 1, matrix("blosum62"))
+    rec, tm = _native.align_host(arena, table, p)
+    assert (rec["status"] == 0).all()
+    pos = rec["score"] > 0
+    assert ((rec["i_end"] < table["a_len"].astype(np.int64)) | ~pos).all()
+    assert ((rec["j_end"] < table["b_len"].astype(np.int64)) | ~pos).all()
+    assert ((rec["matches"] <= rec["aln_len"]) | ~pos).all()
+    pick = np.random.default_rng(2).choice(len(table), 300, replace=False)
+    ref = oracle.align_batch_c(arena, table[pick], 11, 1, matrix("blosum62"), threads=16)
+    got = np.stack([rec[f][pick] for f in FIELDS], axis=1)
+    assert (got == ref[:, :7]).all()
+
+
+def test_pool_overflow_falls_back_exactly():
+    """With a tiny traceback pool, pairs that get no checkpoint room take the
+    scalar + box path and box codes that do not fit are retried: still exact."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+from paper_2303_01845_b200 import _native, workloads, blosum62
+from paper_2303_01845_b200.batch import pack_codes
+from oracle import oracle
+sa, sb = workloads.config3(3000, seed=8)
+arena, table = pack_codes(sa, sb)
+m = np.asarray(blosum62.MATRIX, np.int32)
+rec, tm = _native.align_host(arena, table, _native.make_params(11, 1, m))
+ref = oracle.align_batch_c(arena, table, 11, 1, m, threads=16)
+F = ("score", "i_begin", "i_end", "j_begin", "j_end", "matches", "aln_len")
+got = np.stack([rec[f] for f in F], axis=1)
+print(json.dumps({"bad": int((got != ref[:, :7]).any(axis=1).sum()), "launches": tm["launches"]}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PASTIS_SW_POOL_MB="16")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["bad"] == 0
