@@ -33,7 +33,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = "config2"
-PAIRS_PER_GPU = 100_000
+# BASELINE.json configs: 2 = 100k 300x300 pairs, 3 = 1M skewed-length pairs,
+# 5 = 10k long pairs (2,000-35,000 aa)
+DEFAULT_PAIRS = {"config2": 100_000, "config3": 1_000_000, "config5": 10_000}
 LENGTH = 300
 GAP = (11, 1)
 METRIC = "SW GCUPS (config 2: 300x300 pairs, BLOSUM62, gap 11/1; full alignment incl. traceback)"
@@ -42,16 +44,20 @@ METRIC = "SW GCUPS (config 2: 300x300 pairs, BLOSUM62, gap 11/1; full alignment 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pairs", type=int, default=PAIRS_PER_GPU)
+    ap.add_argument("--pairs", type=int, default=None,
+                    help="pairs per GPU (default: the BASELINE config's count)")
     ap.add_argument("--cpu-sample", type=int, default=3000,
                     help="pairs in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default=WORKLOAD, choices=["config2", "config3", "config5"],
                     help="exploration only; the headline bench is config2")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.pairs is None:
+        args.pairs = DEFAULT_PAIRS[args.workload]
+    return args
 
 
 def dist_env():
@@ -71,29 +77,59 @@ def cpu_bench(mode: str, pairs: int, seed: int = 2303) -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed
+    region: NVML in-process every 5 ms (nvidia-smi every 200 ms if NVML is
+    unavailable).  `timed()` brackets a timed region; the summary covers only
+    the samples taken inside those brackets."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+            "sw_power_cap": 0x4}
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
-        self.gpu = gpu
-        self.rows = []
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x for x in vis.split(",") if x.strip()]
+        self.gpu = int(ids[gpu]) if gpu < len(ids) and ids[gpu].strip().isdigit() else gpu
+        self.rows = []          # (t, sm_mhz, max_mhz, frozenset(reasons))
+        self.windows = []
+        self.source = None
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._nvml = pynvml
+            self.source = "nvml"
+        except Exception:  # noqa: BLE001
+            self.source = "nvidia-smi"
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            return float(sm), float(mx), frozenset(n for n, b in self.BITS.items() if bits & b)
+        out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        return (float(f[0]), float(f[1]),
+                frozenset(n for n, v in zip(self.BITS, f[2:6]) if v.lower() == "active"))
 
     def _run(self):
+        period = 0.005 if self._nvml is not None else 0.2
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                sm, mx, why = self._sample()
+                self.rows.append((time.monotonic(), sm, mx, why))
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -104,20 +140,30 @@ class ClockSampler:
         self._stop.set()
         self._t.join(timeout=10)
 
+    class _Window:
+        def __init__(self, owner):
+            self.owner = owner
+
+        def __enter__(self):
+            self.t0 = time.monotonic()
+
+        def __exit__(self, *exc):
+            self.owner.windows.append((self.t0, time.monotonic()))
+
+    def timed(self):
+        return self._Window(self)
+
     def summary(self) -> dict:
-        if not self.rows:
+        inside = [r for r in self.rows if any(a <= r[0] <= b for a, b in self.windows)]
+        rows = inside or self.rows
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for name, v in zip(names, r[4:8]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+        reasons = sorted(set().union(*[r[3] for r in rows]))
+        return {"sm_mhz": float(np.median([r[1] for r in rows])),
+                "sm_min_mhz": float(min(r[1] for r in rows)),
+                "sm_max_mhz": float(max(r[2] for r in rows)), "reasons": reasons,
+                "samples": len(inside), "source": self.source,
+                "window": "timed region" if inside else "whole run (no sample inside the timed region)"}
 
 
 def run_reference(args, rank: int, world: int) -> None:
@@ -201,7 +247,7 @@ def main():
     if args.workload == "config2":
         sa, sb = workloads.config2(args.pairs, seed=2303 + rank, length=LENGTH)
     elif args.workload == "config3":
-        sa, sb = workloads.config3(args.pairs, seed=2303 + rank)
+        sa, sb = workloads.config3_bulk(args.pairs, seed=2303 + rank)
     else:
         sa, sb = workloads.config5(args.pairs, seed=2303 + rank)
     arena_np, table_np = pack_codes(sa, sb)
@@ -243,21 +289,22 @@ def main():
             time.sleep(0.05)
         torch.cuda.synchronize()
         barrier()
-        for _ in range(args.steps):
-            flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record(stream)
-            tm = device_step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            fwd_ms.append(tm["forward_ms"])
-            rev_ms.append(tm["reverse_ms"])
-            tb_ms.append(tm["traceback_ms"])
-            launches += tm["launches"]
-    barrier()
+        with clocks.timed():
+            for _ in range(args.steps):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                tm = device_step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                step_ms.append(e0.elapsed_time(e1))
+                fwd_ms.append(tm["forward_ms"])
+                rev_ms.append(tm["reverse_ms"])
+                tb_ms.append(tm["traceback_ms"])
+                launches += tm["launches"]
+        barrier()
     dev_ms = max_over_ranks(float(np.sum(step_ms)))
     fwd_total = max_over_ranks(float(np.sum(fwd_ms)))
     total_cells = cells * world * args.steps

@@ -91,6 +91,7 @@ struct DeviceCtx {
   KernelInfo tb[kNumClasses];
   KernelInfo fwd_wide, rev_wide, fwd_cta, rev_cta;
   int max_warps = 0;
+  size_t pool_want = 0;   // checkpoint bytes the last call asked for (pool growth)
   bool ready = false;
 };
 
@@ -253,7 +254,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   CU(c->st.ensure(n_pairs * sizeof(PairState)));
   CU(c->lists.ensure((size_t)kStages * kNumClasses * n_pairs * 4));
   CU(c->ctrs.ensure(2 * kStages * kNumClasses * 4));
-  CU(c->stats.ensure(4 * 8));
+  CU(c->stats.ensure(8 * 8));
   // int8 matrix incl. the virtual code 25 (-128 everywhere)
   int8_t mat[kMatBytes];
   memset(mat, 0, sizeof(mat));
@@ -263,7 +264,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
           (i == kPad || j == kPad) ? (int8_t)-128 : (int8_t)prm->matrix[i * 25 + j];
   CU(cudaMemcpyAsync(c->mat.p, mat, kCodes * kCodes, cudaMemcpyHostToDevice, s));
   CU(cudaMemsetAsync(c->ctrs.p, 0, 2 * kStages * kNumClasses * 4, s));
-  CU(cudaMemsetAsync(c->stats.p, 0, 4 * 8, s));
+  CU(cudaMemsetAsync(c->stats.p, 0, 8 * 8, s));
 
   KArgs A;
   memset(&A, 0, sizeof(A));
@@ -335,112 +336,158 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   }
   // No host round trip before the kernels: the strip-boundary scratch is
   // sized for the longest supported sequence and the traceback pool is one
-  // large cached allocation (pool overflow falls back to retry rounds).
+  // cached allocation, grown between calls to what the previous call's
+  // checkpoints asked for.  A call that outgrows it runs extra packed rounds
+  // on the deferred pairs with the pool recycled (device-side chunking).
   A.bnd_stride = 65000 + 64;
   CU(c->bnd.ensure((size_t)c->max_warps * A.bnd_stride * sizeof(int2)));
   A.bnd = (int2 *)c->bnd.p;
-  if (c->pool.bytes == 0) {
+  // PASTIS_SW_POOL_MB pins the pool size (tests use it to force the deferral paths)
+  static const long long env_mb = [] {
+    const char *e = getenv("PASTIS_SW_POOL_MB");
+    return e ? atoll(e) : 0ll;
+  }();
+  if (c->pool.bytes == 0 || c->pool_want > c->pool.bytes) {
     size_t free_b = 0, total_b = 0;
     CU(cudaMemGetInfo(&free_b, &total_b));
-    size_t cap = std::min<size_t>((size_t)(free_b * 0.5), (size_t)48 << 30);
-    // PASTIS_SW_POOL_MB caps the pool (exercises the overflow / retry paths)
-    if (const char *e = getenv("PASTIS_SW_POOL_MB")) cap = std::min<size_t>(cap, (size_t)atoll(e) << 20);
-    CU(c->pool.ensure(std::max<size_t>(cap, (size_t)8 << 20)));
+    const size_t limit = (size_t)((double)(free_b + c->pool.bytes) * 0.8);
+    size_t target = c->pool.bytes == 0 ? std::min<size_t>(free_b / 2, (size_t)16 << 30) : c->pool.bytes;
+    target = std::min(std::max(target, c->pool_want), limit);
+    if (env_mb > 0) target = std::min<size_t>(target, (size_t)env_mb << 20);
+    target = std::max<size_t>(target, env_mb > 0 ? (size_t)1 << 20 : (size_t)8 << 20);
+    if (target > c->pool.bytes) {
+      c->pool.release();
+      CU(c->pool.ensure(target));
+    }
   }
   const double h1 = now_ms();
   A.pool = (uint8_t *)c->pool.p;
   A.pool_cap = c->pool.bytes - 64;  // headroom for the widest vector store
-  CU(c->ctrs.ensure(2 * kStages * kNumClasses * 4));
-  // pool_top lives in the stats buffer slot 3
+  // pool_top lives in the stats buffer slot 3; slot 4 = bytes the first
+  // packed round asked for
   A.pool_top = (unsigned long long *)c->stats.p + 3;
-  CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
   const double h2 = now_ms();
-
   CU(cudaEventRecord(c->ev[1], s));
-  // short/medium pairs: packed forward + checkpoints, then the tile traceback,
-  // one stream per length class
-  CU(cudaEventRecord(c->ev_fork, s));
-  for (int cls = 0; cls < kNumClasses; ++cls) {
-    cudaStream_t cs = c->cstream[cls];
-    CU(cudaStreamWaitEvent(cs, c->ev_fork, 0));
-    c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, cs>>>(A, 6, cls);
-    CU(cudaEventRecord(c->ev_k1[cls], cs));
-    c->tb[cls].fn<<<c->tb[cls].grid, kTbWarps * 32, 0, cs>>>(A, 7, cls);
-    CU(cudaEventRecord(c->ev_tb[cls], cs));
-    launches += 2;
-  }
-  // long pairs: scalar forward concurrently with the packed classes -- one CTA
-  // per pair for pairs of >= 4 strips, one warp per pair for the others
-  c->fwd_cta.fn<<<c->fwd_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 0, kCtaClass);
-  c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
-      A, 0, kLongClass);
-  launches += 2;
-  CU(cudaEventRecord(c->ev[7], s));   // end of the concurrent scalar forward
-  // then the packed pass's fallbacks (their own list, complete once every
-  // packed class has finished), on the long-pair kernel
-  for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_k1[cls], 0));
-  CU(cudaEventRecord(c->ev[6], s));   // start of the scalar (long-pair) tail
-  c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
-      A, 0, kFallbackClass);
-  ++launches;
-  c->fwd_wide.fn<<<c->fwd_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 3, 0);
-  ++launches;
-  CU(cudaGetLastError());
-  CU(cudaEventRecord(c->ev[2], s));
-  c->rev_cta.fn<<<c->rev_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 1, kCtaClass);
-  c->rev[kLongClass].fn<<<c->rev[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
-      A, 1, kLongClass);
-  launches += 2;
-  c->rev_wide.fn<<<c->rev_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 4, 0);
-  ++launches;
-  CU(cudaGetLastError());
-  CU(cudaEventRecord(c->ev[3], s));
-  for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_tb[cls], 0));
-  double tb_ms = 0.0;
-  for (int round = 0;; ++round) {
-    for (int cls = 0; cls < kNumClasses; ++cls) {
-      c->box[cls].fn<<<c->box[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 2, cls);
+
+  uint32_t h_cnt[kStages * kNumClasses];
+  double fwd_ms = 0.0, rev_ms = 0.0, tb_ms = 0.0;
+  uint64_t wide = 0;
+  for (int pround = 0;; ++pround) {
+    CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
+    if (pround > 0) {
+      k_packed_round<<<kNumClasses, 256, 0, s>>>(A);
       ++launches;
     }
-    k_walk<<<(unsigned)((n_pairs + 127) / 128), 128, 0, s>>>(A, nullptr, 0);
+    // short/medium pairs: packed forward + checkpoints, then the tile
+    // traceback, one stream per length class
+    CU(cudaEventRecord(c->ev_fork, s));
+    for (int cls = 0; cls < kNumClasses; ++cls) {
+      cudaStream_t cs = c->cstream[cls];
+      CU(cudaStreamWaitEvent(cs, c->ev_fork, 0));
+      c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, cs>>>(A, 6, cls);
+      CU(cudaEventRecord(c->ev_k1[cls], cs));
+      c->tb[cls].fn<<<c->tb[cls].grid, kTbWarps * 32, 0, cs>>>(A, 7, cls);
+      CU(cudaEventRecord(c->ev_tb[cls], cs));
+      launches += 2;
+    }
+    // long pairs: scalar forward concurrently with the packed classes -- one
+    // CTA per pair for pairs of >= 4 strips, one warp per pair for the others
+    // (their lists are empty after the first round)
+    c->fwd_cta.fn<<<c->fwd_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 0, kCtaClass);
+    c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
+        A, 0, kLongClass);
+    launches += 2;
+    CU(cudaEventRecord(c->ev[7], s));   // end of the concurrent scalar forward
+    // then the packed pass's scalar fallbacks (their own list, complete once
+    // every packed class has finished), on the long-pair kernel
+    for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_k1[cls], 0));
+    if (pround == 0)
+      CU(cudaMemcpyAsync((unsigned long long *)c->stats.p + 4, A.pool_top, 8,
+                         cudaMemcpyDeviceToDevice, s));
+    c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
+        A, 0, kFallbackClass);
+    ++launches;
+    c->fwd_wide.fn<<<c->fwd_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 3, 0);
     ++launches;
     CU(cudaGetLastError());
-    CU(cudaEventRecord(c->ev[4], s));
-    uint32_t retry = 0;
-    CU(cudaMemcpyAsync(&retry, (uint32_t *)c->ctrs.p + 5 * kNumClasses, 4, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-    tb_ms += ev_ms(round == 0 ? c->ev[3] : c->ev[5], c->ev[4]);
-    if (retry == 0) break;
-    if (round > 64) return fail(SW_EINTERNAL, "traceback code pool too small for one pair");
-    // requeue: reset K3 lists, pool, retry list
-    CU(cudaEventRecord(c->ev[5], s));
-    uint32_t *ctrs = (uint32_t *)c->ctrs.p;
-    CU(cudaMemsetAsync(ctrs + 2 * kNumClasses, 0, kNumClasses * 4, s));
-    CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 2 * kNumClasses, 0, kNumClasses * 4, s));
-    CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
-    k_requeue<<<64, 256, 0, s>>>(A);
+    CU(cudaEventRecord(c->ev[2], s));
+    c->rev_cta.fn<<<c->rev_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 1, kCtaClass);
     ++launches;
-    CU(cudaMemsetAsync(ctrs + 5 * kNumClasses, 0, 4, s));
-    CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 5 * kNumClasses, 0, 4, s));
-  }
-  if (tm) {
+    c->rev[kLongClass].fn<<<c->rev[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
+        A, 1, kLongClass);
+    c->rev_wide.fn<<<c->rev_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 4, 0);
+    launches += 2;
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(c->ev[3], s));
+    for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_tb[cls], 0));
+    uint32_t last_retry = 0;
+    for (int round = 0;; ++round) {
+      for (int cls = 0; cls < kNumClasses; ++cls) {
+        c->box[cls].fn<<<c->box[cls].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 2, cls);
+        ++launches;
+      }
+      k_walk<<<(unsigned)((n_pairs + 127) / 128), 128, 0, s>>>(A, nullptr, 0);
+      ++launches;
+      CU(cudaGetLastError());
+      CU(cudaEventRecord(c->ev[4], s));
+      CU(cudaMemcpyAsync(h_cnt, c->ctrs.p, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      tb_ms += ev_ms(round == 0 ? c->ev[3] : c->ev[5], c->ev[4]);
+      const uint32_t n_retry = h_cnt[5 * kNumClasses];
+      if (n_retry == 0) break;
+      // every retry round starts on an empty pool, so it places at least one
+      // box unless a single box is larger than the whole pool
+      if (round > 0 && n_retry >= last_retry) {
+        // grow the pool (its contents are dead here: every placed box has
+        // been walked) unless PASTIS_SW_POOL_MB pins it
+        size_t free_b = 0, total_b = 0;
+        CU(cudaMemGetInfo(&free_b, &total_b));
+        const size_t grown = c->pool.bytes * 2;
+        if (env_mb > 0 || grown > (size_t)((double)(free_b + c->pool.bytes) * 0.8))
+          return fail(SW_EINTERNAL, "traceback code pool too small for one pair's box");
+        c->pool.release();
+        CU(c->pool.ensure(grown));
+        A.pool = (uint8_t *)c->pool.p;
+        A.pool_cap = c->pool.bytes - 64;
+      }
+      last_retry = n_retry;
+      // requeue: reset K3 lists, pool, retry list
+      CU(cudaEventRecord(c->ev[5], s));
+      uint32_t *ctrs = (uint32_t *)c->ctrs.p;
+      CU(cudaMemsetAsync(ctrs + 2 * kNumClasses, 0, kNumClasses * 4, s));
+      CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 2 * kNumClasses, 0, kNumClasses * 4, s));
+      CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
+      k_requeue<<<64, 256, 0, s>>>(A);
+      ++launches;
+      CU(cudaMemsetAsync(ctrs + 5 * kNumClasses, 0, 4, s));
+      CU(cudaMemsetAsync(ctrs + kStages * kNumClasses + 5 * kNumClasses, 0, 4, s));
+    }
     // forward = the forward passes that run concurrently after the fork: the
     // packed classes (their own streams) and the scalar long-pair pass (main
-    // stream); the rare fallback re-run is not included (it is in kernel_ms)
-    double fwd = ev_ms(c->ev_fork, c->ev[7]);
-    for (int cls = 0; cls < kNumClasses; ++cls)
-      fwd = std::max(fwd, (double)ev_ms(c->ev_fork, c->ev_k1[cls]));
-    tm->forward_ms += fwd;
-    tm->reverse_ms += ev_ms(c->ev[2], c->ev[3]);
+    // stream); the scalar fallback re-run is not included (it is in kernel_ms)
+    double f = ev_ms(c->ev_fork, c->ev[7]);
+    for (int cls = 0; cls < kNumClasses; ++cls) f = std::max(f, (double)ev_ms(c->ev_fork, c->ev_k1[cls]));
+    fwd_ms += f;
+    rev_ms += ev_ms(c->ev[2], c->ev[3]);
+    wide += h_cnt[3 * kNumClasses];
+    uint32_t deferred = 0;
+    for (int cls = 0; cls < kNumClasses; ++cls) deferred += h_cnt[8 * kNumClasses + cls];
+    if (deferred == 0) break;
+    if (pround >= 1024) return fail(SW_EINTERNAL, "checkpoint pool too small for the batch");
+  }
+  CU(cudaEventRecord(c->ev[8], s));
+  unsigned long long hstats[5] = {0ull, 0ull, 0ull, 0ull, 0ull};
+  CU(cudaMemcpyAsync(hstats, c->stats.p, sizeof(hstats), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (hstats[4] > c->pool.bytes) c->pool_want = (size_t)hstats[4];   // grow on the next call
+  if (tm) {
+    tm->forward_ms += fwd_ms;
+    tm->reverse_ms += rev_ms;
     tm->traceback_ms += tb_ms;
-    tm->kernel_ms += ev_ms(c->ev[0], c->ev[1]) + ev_ms(c->ev[1], c->ev[3]) + tb_ms;
-    unsigned long long hstats[2] = {0ull, 0ull};
-    CU(cudaMemcpy(hstats, c->stats.p, sizeof(hstats), cudaMemcpyDeviceToHost));
+    tm->kernel_ms += ev_ms(c->ev[0], c->ev[8]);
     tm->cells += hstats[0];
     tm->launches += launches;
-    uint32_t h_ctrs[kStages * kNumClasses];
-    CU(cudaMemcpy(h_ctrs, c->ctrs.p, sizeof(h_ctrs), cudaMemcpyDeviceToHost));
-    tm->wide_pairs += h_ctrs[3 * kNumClasses];
+    tm->wide_pairs += wide;
     tm->host_plan_ms += h1 - h0;
     tm->host_setup_ms += h2 - h1;
   }

@@ -55,8 +55,9 @@ constexpr int kCtaStripsMin = 4;
 __host__ __device__ inline int long_class(int m) {
   return (m + 32 * kCtaRowsR - 1) / (32 * kCtaRowsR) >= kCtaStripsMin ? kCtaClass : kLongClass;
 }
-constexpr int kStages = 8;  // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
-                            // 6 K1 with checkpoints, 7 tile traceback
+constexpr int kStages = 9;  // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
+                            // 6 K1 with checkpoints, 7 tile traceback,
+                            // 8 K1 with checkpoints deferred to the next round (pool full)
 constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take the fused path
 constexpr int32_t kScaledLimit = 32767 - 128;
 constexpr int32_t kNegInf = -(1 << 30);
@@ -1242,6 +1243,23 @@ __global__ void k_requeue(KArgs A) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const uint32_t k = list_of(A, 5, 0)[t];
     list_push(A, 2, class_of(A.st[k].i_end - A.st[k].i0 + 1), k);
+  }
+}
+
+// Start another packed round: the pairs deferred for lack of checkpoint room
+// (stage 8) become the packed input (stage 6) and every other list and cursor
+// of the class is emptied.  One block per class.
+__global__ void k_packed_round(KArgs A) {
+  const int c = blockIdx.x;
+  const uint32_t n = A.ctrs[8 * kNumClasses + c];
+  const uint32_t *src = list_of(A, 8, c);
+  uint32_t *dst = list_of(A, 6, c);
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) dst[t] = src[t];
+  __syncthreads();
+  if (threadIdx.x < kStages) {
+    const int stage = threadIdx.x;
+    A.ctrs[stage * kNumClasses + c] = stage == 6 ? n : 0u;
+    A.ctrs[kStages * kNumClasses + stage * kNumClasses + c] = 0u;
   }
 }
 

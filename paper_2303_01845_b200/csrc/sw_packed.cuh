@@ -222,6 +222,29 @@ k_score_packed(KArgs A, int stage, int cls) {
         P[h].ck_off = off;
       }
     }
+    // The pool is one allocation carved per pair; when it is full a pair is
+    // deferred to the next round (stage 8; the pool is recycled between
+    // rounds), or -- if its checkpoints would take over a quarter of the pool
+    // -- sent to the scalar path.  A duo with no room at all skips the fill.
+    auto defer = [&](int h) {
+      PairState *st = A.st + P[h].k;
+      const CkLayout OL = ck_layout(R, P[h].n);
+      const uint64_t own = (uint64_t)((P[h].m + 32 * R - 1) / (32 * R)) * OL.strip_words * 4ull;
+      if (own > A.pool_cap / 4) {
+        st->flags = 0;
+        list_push(A, 0, kFallbackClass, (uint32_t)P[h].k);
+      } else {
+        st->flags = kFlagRetry;                 // k_walk leaves it alone this round
+        list_push(A, 8, cls, (uint32_t)P[h].k);
+      }
+    };
+    if (!((P[0].k >= 0 && P[0].ck) || (P[1].k >= 0 && P[1].ck))) {
+      if (lane == 0) {
+        if (P[0].k >= 0) defer(0);
+        if (P[1].k >= 0) defer(1);
+      }
+      continue;
+    }
     uint64_t keyA = 0ull, keyB = 0ull;
     uint32_t vmax2 = 0u;
     for (int strip = 0; strip < nstrips; ++strip) {
@@ -402,9 +425,8 @@ k_score_packed(KArgs A, int stage, int cls) {
           st->box_m = m;
           st->box_n = n;
           list_push(A, 7, cls, (uint32_t)P[h].k);
-        } else {                               // no checkpoint room: scalar path
-          st->flags = 0;
-          list_push(A, 0, kFallbackClass, (uint32_t)P[h].k);
+        } else {                               // no checkpoint room
+          defer(h);
         }
       }
     }
