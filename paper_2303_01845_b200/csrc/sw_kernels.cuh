@@ -772,6 +772,7 @@ constexpr int16_t kNeg16 = -16384;  // boundary "-inf": below -open - ext for op
 
 struct TbSmem {
   int16_t H[33][kTbX], E[33][kTbX], F[33][kTbX];  // row 0 / col 0 = halo
+  uint4 row[32];        // per tile row: (Ho, E) and (diag above, F_bot) at c_lo - 1, matrix row
   uint8_t bcode[kTbX], braw[kTbX];
   uint8_t acode[32], araw[32];
 };
@@ -885,34 +886,61 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
       if (idx >= 0) pf(row + idx);
     }
   }
-  // row-to-row hand-off: (Ho, F) of the row above as one packed int16 pair
-  uint32_t out = ((uint32_t)Ho & 0xFFFFu) | ((uint32_t)((rq == R - 1) ? FbotT : (int32_t)kNeg16) << 16);
-  const int32_t hoAbove = __shfl_up_sync(0xffffffffu, Ho, 1);
-  int32_t prevTop = (rq == 0) ? hoUpPrevT : hoAbove;
-  const int vstart = q - q / R;
-  const int vlast = min(qmax - qmax / R + 31, kap_in - (32 * w - t0) + qmax);
-  const int xbase = (32 * w - t0) - q - cmin + 1;   // x = xbase + v
-  const int8_t *mrow = smat + acode * kCodes;
+  // Column-parallel replay: lane l owns column c_lo(row) + l and the warp
+  // steps down the tile one row at a time (no wavefront skew).  Per row:
+  //   F  = max(F_up - ext, H_up - open)            (vertical, from the row above)
+  //   Ht = max(0, H_diag + s, F)                     (H without the horizontal term)
+  //   E  = horizontal gap, exactly E[l] = max(E[l-1] - ext, H[l-1] - open), as a
+  //        max-plus prefix scan over the lanes: with open >= ext,
+  //        E[l] + l*ext = max(E[0], max_{l'<l} Ht[l'] - open + (l'+1)*ext)
+  //   H  = max(Ht, E)
+  // Rows of forward lane t cover columns 32w - t + [0, 32): entering the next
+  // forward lane shifts the columns left by one, so the row above is shifted
+  // one lane up; its lane-0 cell and the diagonal come from the checkpoints.
+  if (row_ok)
+    T.row[q] = make_uint4(((uint32_t)Ho & 0xFFFFu) | ((uint32_t)E << 16),
+                          ((uint32_t)hoUpPrevT & 0xFFFFu) | ((uint32_t)FbotT << 16),
+                          (uint32_t)(acode * kCodes), 0u);
+  int32_t upH = (int32_t)(int16_t)(topv & 0xFFFFu) + OPEN, upF = (int32_t)topv >> 16;
+  int32_t prevHb = 0, prevFb = kNeg16;   // H / F of the previous row at ITS c_lo - 1
+  const int32_t Kl = (lane + 1) * EXT - OPEN, lext = lane * EXT;
   __syncwarp();
-#pragma unroll 2
-  for (int v = 0; v <= vlast; ++v) {
-    const uint32_t up = __shfl_up_sync(0xffffffffu, out, 1);
-    const uint32_t tv = __shfl_sync(0xffffffffu, topv, v & 31);
-    const uint32_t in = q == 0 ? tv : up;
-    const int32_t topHo = (int32_t)(int16_t)(in & 0xFFFFu), topF = (int32_t)in >> 16;
-    const int x = xbase + v;
-    if (row_ok & (v >= vstart) & (v <= vstart + 31)) {
-      const int32_t sc = mrow[T.bcode[x - 1]];
-      const int32_t e = max(E - EXT, Ho);
-      const int32_t f = max(topF - EXT, topHo);
-      const int32_t h = __vimax3_s32_relu(prevTop + sc + OPEN, e, f);
-      T.H[q + 1][x] = (int16_t)h;
-      T.E[q + 1][x] = (int16_t)e;
-      T.F[q + 1][x] = (int16_t)f;
-      E = e;
-      Ho = h - OPEN;
-      out = ((uint32_t)Ho & 0xFFFFu) | ((uint32_t)f << 16);
-      prevTop = topHo;
+  int qq = 0;
+  for (int tb = t0; qq <= qmax; ++tb) {     // forward lanes of the tile
+    if (qq > 0) {                           // columns shift left by one: row above one lane up
+      const int32_t sh = __shfl_up_sync(0xffffffffu, upH, 1);
+      const int32_t sf = __shfl_up_sync(0xffffffffu, upF, 1);
+      upH = lane == 0 ? prevHb : sh;
+      upF = lane == 0 ? prevFb : sf;
+    }
+    const int xs = (t1 - tb) + 1 + lane;    // tile column of this lane's cell
+    const int8_t *mcol = smat + T.bcode[xs - 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (qq > qmax) break;
+      const uint4 rw = T.row[qq];            // broadcast
+      const int32_t HbO = (int32_t)(int16_t)(rw.x & 0xFFFFu), Eb = (int32_t)rw.x >> 16;
+      int32_t dg = __shfl_up_sync(0xffffffffu, upH, 1);
+      if (lane == 0) dg = r == 0 ? (int32_t)(int16_t)(rw.y & 0xFFFFu) + OPEN : prevHb;
+      const int32_t sc = mcol[rw.z];
+      const int32_t f = max(upF - EXT, upH - OPEN);
+      const int32_t ht = __vimax3_s32_relu(dg + sc, f, 0);
+      int32_t z = ht + Kl;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) z = max(z, (int32_t)__shfl_up_sync(0xffffffffu, z, d));
+      int32_t ex = __shfl_up_sync(0xffffffffu, z, 1);
+      const int32_t x0e = max(Eb - EXT, HbO);               // E at c_lo (left boundary)
+      if (lane == 0) ex = x0e;
+      const int32_t e = max(x0e, ex) - lext;
+      const int32_t h = max(ht, e);
+      T.H[qq + 1][xs] = (int16_t)h;
+      T.E[qq + 1][xs] = (int16_t)e;
+      T.F[qq + 1][xs] = (int16_t)f;
+      upH = h;
+      upF = f;
+      prevHb = HbO + OPEN;
+      prevFb = (int32_t)rw.y >> 16;
+      ++qq;
     }
   }
   __syncwarp();
@@ -921,12 +949,16 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
 template <int R>
 __global__ void __launch_bounds__(kTbWarps * 32)
 k_tb(KArgs A, int stage, int cls) {
-  __shared__ int8_t smat[kCodes * kCodes];
-  __shared__ TbSmem tsm[kTbWarps];
+  struct Shared {
+    TbSmem t[kTbWarps];
+    int8_t mat[kCodes * kCodes];
+  };
+  __shared__ __align__(16) Shared sh;   // one shared window base for tiles and matrix
+  int8_t *smat = sh.mat;
   for (int i = threadIdx.x; i < kCodes * kCodes; i += blockDim.x) smat[i] = A.mat[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  TbSmem &T = tsm[warp];
+  TbSmem &T = sh.t[warp];
   const int32_t OPEN = A.open_, EXT = A.ext, Bias = A.bias16;
   for (;;) {
     const int64_t k = next_item(A, stage, cls, lane);
