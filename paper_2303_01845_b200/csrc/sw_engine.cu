@@ -92,8 +92,16 @@ struct DeviceCtx {
   KernelInfo fwd_wide, rev_wide, fwd_cta, rev_cta;
   int max_warps = 0;
   size_t pool_want = 0;   // checkpoint bytes the last call asked for (pool growth)
+  // host path: the arena is uploaded in slices on copy_stream while the packed
+  // forward already runs; `ready` counts the slices that have landed
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_pairs = nullptr, ev_arena = nullptr;
+  DevBuf readyb;
+  uint32_t *slice_vals = nullptr;   // pinned 1..kMaxSlices
   bool ready = false;
 };
+
+constexpr int kMaxSlices = 64;
 
 std::mutex g_ctx_mu;
 std::vector<DeviceCtx *> g_ctx;
@@ -189,6 +197,12 @@ int get_ctx(int device, DeviceCtx **out) {
       CU(cudaEventCreate(&c->ev_k1[k]));
       CU(cudaEventCreateWithFlags(&c->ev_tb[k], cudaEventDisableTiming));
     }
+    CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&c->ev_pairs, cudaEventDisableTiming));
+    CU(cudaEventCreate(&c->ev_arena));
+    CU(c->readyb.ensure(64));
+    CU(cudaHostAlloc((void **)&c->slice_vals, kMaxSlices * sizeof(uint32_t), cudaHostAllocDefault));
+    for (int k = 0; k < kMaxSlices; ++k) c->slice_vals[k] = (uint32_t)(k + 1);
     int rc = setup_classes<0>(c);
     if (rc) return rc;
     rc = setup_kernel(k_score<16, 0, true>, c->sms, c->fwd_wide, c->max_warps);
@@ -242,9 +256,14 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 }
 
 // Core device pipeline.  Caller holds c->mu and has set the device.
+// `ready`/`slice_bytes`/`arena_done`: host-pipelined arena (align_host) --
+// the packed forward waits per pair for its slices, everything reading the
+// encoded arena waits for arena_done; nullptr = the arena is resident.
 int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
                const sw_pair_t *d_pairs, uint64_t n_pairs, const sw_params_t *prm,
-               sw_result_t *d_out, cudaStream_t s, sw_timing_t *tm) {
+               sw_result_t *d_out, cudaStream_t s, sw_timing_t *tm,
+               const uint32_t *ready = nullptr, uint64_t slice_bytes = 0,
+               cudaEvent_t arena_done = nullptr) {
   if (n_pairs == 0) return SW_OK;
   if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
   uint32_t launches = 0;
@@ -277,6 +296,9 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   A.lists = (uint32_t *)c->lists.p;
   A.ctrs = (uint32_t *)c->ctrs.p;
   A.n_pairs = n_pairs;
+  A.lut = (const uint8_t *)c->lut.p;
+  A.ready = ready;
+  A.slice_bytes = slice_bytes;
   A.open_ = prm->gap_open;
   A.ext = prm->gap_extend;
   int smin = 127, smax = -128;
@@ -295,12 +317,14 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   const bool packed_ok = smax - A.prof_lo <= 127;
 
   CU(cudaEventRecord(c->ev[0], s));
-  {
+  if (!arena_done) {   // resident arena: encode first, every kernel reads codes
     const int threads = 256;
     uint64_t blocks = std::min<uint64_t>((arena_bytes / 16 + threads) / threads + 1, (uint64_t)c->sms * 8);
     k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, (uint8_t *)c->codes.p, arena_bytes,
                                                  (const uint8_t *)c->lut.p);
     ++launches;
+  }
+  {
     // PASTIS_SW_TRACEBACK=box forces the reverse-pass + box traceback for every
     // pair (A/B comparisons); default: checkpoint + tile replay for pairs
     // up to kFusedMaxCells cells.
@@ -390,6 +414,17 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
       CU(cudaEventRecord(c->ev_tb[cls], cs));
       launches += 2;
     }
+    if (pround == 0 && arena_done) {
+      // host-pipelined arena: the packed pass reads raw bytes through the
+      // LUT; the scalar kernels below read the encoded arena once all of it
+      // has landed
+      CU(cudaStreamWaitEvent(s, arena_done, 0));
+      const int threads = 256;
+      uint64_t blocks = std::min<uint64_t>((arena_bytes / 16 + threads) / threads + 1, (uint64_t)c->sms * 8);
+      k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, (uint8_t *)c->codes.p, arena_bytes,
+                                                   (const uint8_t *)c->lut.p);
+      ++launches;
+    }
     // long pairs: scalar forward concurrently with the packed classes -- one
     // CTA per pair for pairs of >= 4 strips, one warp per pair for the others
     // (their lists are empty after the first round)
@@ -475,7 +510,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     if (deferred == 0) break;
     if (pround >= 1024) return fail(SW_EINTERNAL, "checkpoint pool too small for the batch");
   }
-  CU(cudaEventRecord(c->ev[8], s));
+  CU(cudaEventRecord(c->ev[12], s));
   unsigned long long hstats[5] = {0ull, 0ull, 0ull, 0ull, 0ull};
   CU(cudaMemcpyAsync(hstats, c->stats.p, sizeof(hstats), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
@@ -484,7 +519,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     tm->forward_ms += fwd_ms;
     tm->reverse_ms += rev_ms;
     tm->traceback_ms += tb_ms;
-    tm->kernel_ms += ev_ms(c->ev[0], c->ev[8]);
+    tm->kernel_ms += ev_ms(c->ev[0], c->ev[12]);
     tm->cells += hstats[0];
     tm->launches += launches;
     tm->wide_pairs += wide;
@@ -518,19 +553,36 @@ int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_
   CU(c->arena.ensure(arena_bytes + 64));
   CU(c->pairs.ensure(n_pairs * sizeof(sw_pair_t)));
   CU(c->out.ensure(n_pairs * sizeof(sw_result_t)));
+  // Upload on the copy stream: the pair table first (the planning kernels
+  // need it), then the arena in slices, each followed by a 4-byte copy that
+  // bumps `ready`; the packed forward starts as soon as its pairs' slices
+  // have landed, so the arena upload overlaps the forward pass.
+  cudaStream_t cs = c->copy_stream;
+  const uint64_t slice = std::max<uint64_t>((uint64_t)4 << 20,
+                                            (arena_bytes + kMaxSlices - 1) / kMaxSlices);
+  const int nslices = (int)((arena_bytes + slice - 1) / slice);
   CU(cudaEventRecord(c->ev[8], s));
-  CU(cudaMemcpyAsync(c->arena.p, arena, arena_bytes, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(c->pairs.p, pairs, n_pairs * sizeof(sw_pair_t), cudaMemcpyHostToDevice, s));
-  CU(cudaEventRecord(c->ev[9], s));
+  CU(cudaStreamWaitEvent(cs, c->ev[8], 0));
+  CU(cudaMemsetAsync(c->readyb.p, 0, 4, cs));
+  CU(cudaMemcpyAsync(c->pairs.p, pairs, n_pairs * sizeof(sw_pair_t), cudaMemcpyHostToDevice, cs));
+  CU(cudaEventRecord(c->ev_pairs, cs));
+  for (int k = 0; k < nslices; ++k) {
+    const uint64_t b0 = (uint64_t)k * slice, nb = std::min<uint64_t>(slice, arena_bytes - b0);
+    CU(cudaMemcpyAsync((uint8_t *)c->arena.p + b0, arena + b0, nb, cudaMemcpyHostToDevice, cs));
+    CU(cudaMemcpyAsync(c->readyb.p, c->slice_vals + k, 4, cudaMemcpyHostToDevice, cs));
+  }
+  CU(cudaEventRecord(c->ev_arena, cs));
+  CU(cudaStreamWaitEvent(s, c->ev_pairs, 0));
   rc = run_device(c, (const uint8_t *)c->arena.p, arena_bytes, (const sw_pair_t *)c->pairs.p,
-                  n_pairs, params, (sw_result_t *)c->out.p, s, tm);
+                  n_pairs, params, (sw_result_t *)c->out.p, s, tm,
+                  nslices > 0 ? (const uint32_t *)c->readyb.p : nullptr, slice, c->ev_arena);
   if (rc) return rc;
   CU(cudaEventRecord(c->ev[10], s));
   CU(cudaMemcpyAsync(out, c->out.p, n_pairs * sizeof(sw_result_t), cudaMemcpyDeviceToHost, s));
   CU(cudaEventRecord(c->ev[11], s));
   CU(cudaStreamSynchronize(s));
   if (tm) {
-    tm->h2d_ms = ev_ms(c->ev[8], c->ev[9]);
+    tm->h2d_ms = ev_ms(c->ev[8], c->ev_arena);   // overlaps the forward pass
     tm->d2h_ms = ev_ms(c->ev[10], c->ev[11]);
     tm->h2d_bytes = arena_bytes + n_pairs * sizeof(sw_pair_t);
     tm->d2h_bytes = n_pairs * sizeof(sw_result_t);
@@ -685,6 +737,7 @@ void sw_release(int device) {
     for (DevBuf *b : {&c->arena, &c->codes, &c->pairs, &c->out, &c->st, &c->lists, &c->ctrs,
                       &c->stats, &c->bnd, &c->pool, &c->skeys, &c->svals, &c->cubtmp})
       b->release();
+    c->pool_want = 0;
   }
 }
 

@@ -98,6 +98,11 @@ struct KArgs {
   uint32_t *lists;         // [kStages][kNumClasses][n_pairs]
   uint32_t *ctrs;          // count[kStages*kNumClasses], cursor[...] after it
   uint64_t n_pairs;
+  const uint8_t *lut;      // raw byte -> residue code (align.py:27-30), 256 entries
+  // host-pipelined arenas: ready = number of arena slices of slice_bytes that
+  // have landed (written by the copy stream); nullptr = arena fully resident
+  const volatile uint32_t *ready;
+  uint64_t slice_bytes;
   int2 *bnd;               // per-warp strip boundary rows
   uint64_t bnd_stride;     // int2 per warp
   uint8_t *pool;           // traceback code pool
@@ -152,6 +157,27 @@ struct View {
   int step;
   __device__ __forceinline__ int at(int x) const { return p[(int64_t)step * x]; }
 };
+// The packed forward's sequence view.  Resident arena: p = encoded codes,
+// lut = nullptr.  Host-pipelined arena: p = RAW bytes encoded on the fly
+// (lut[raw]) with L1-bypassing loads, since slices may still be arriving
+// while the kernel runs (A.ready).
+struct RawView {
+  const uint8_t *p;
+  const uint8_t *lut;
+  __device__ __forceinline__ int at(int x) const {
+    return lut ? (int)__ldg(lut + __ldcg(p + x)) : (int)__ldg(p + x);
+  }
+};
+// Wait until the arena slices holding [0, end) have landed (no-op when the
+// arena is resident).  Lane 0 spins; the copy stream needs no SM.
+__device__ __forceinline__ void wait_arena(const KArgs &A, uint64_t end, int lane) {
+  if (A.ready == nullptr || end == 0) return;
+  if (lane == 0) {
+    const uint32_t need = (uint32_t)((end - 1) / A.slice_bytes + 1);
+    while (*A.ready < need) __nanosleep(256);
+  }
+  __syncwarp();
+}
 
 // Build this lane's slice of the query profile for rows row0+lane*R .. +R-1.
 template <int R>
@@ -784,7 +810,7 @@ __device__ __forceinline__ int32_t uhi(uint32_t x, int32_t B) { return (int32_t)
 template <int R>
 __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const uint32_t *ck,
                                           const CkLayout &CL, int strip, int g, int w, int m,
-                                          int n, const uint8_t *acodes, const uint8_t *bcodes,
+                                          int n, const RawView &acodes, const RawView &bcodes,
                                           const uint8_t *araw, const uint8_t *braw, int lane,
                                           int32_t OPEN, int32_t EXT, int32_t B, int &trow0,
                                           int &tcmin, const int rho_in, const int kap_in) {
@@ -798,8 +824,9 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
   for (int x = lane; x < width; x += 32) {
     const int c = cmin + x;
     const bool ok = (c >= 0) & (c < n);
-    T.bcode[x] = ok ? bcodes[c] : (uint8_t)kPad;
-    T.braw[x] = ok ? braw[c] : (uint8_t)0;
+    const uint8_t rb = ok ? __ldcg(braw + c) : (uint8_t)0;
+    T.bcode[x] = ok ? (uint8_t)__ldg(bcodes.lut + rb) : (uint8_t)kPad;
+    T.braw[x] = rb;
   }
   // the walk enters at (rho_in, kap_in) and only moves up/left
   const int qmax = rho_in - trow0;
@@ -808,10 +835,11 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
   const int tq = t0 + q / R, rq = q - (q / R) * R;
   const int rho = trow0 + q;
   const bool real_row = row_ok & (rho < m);
-  const int acode = real_row ? acodes[rho] : kPad;
+  const uint8_t ra = real_row ? __ldcg(araw + rho) : (uint8_t)0;
+  const int acode = real_row ? (int)__ldg(acodes.lut + ra) : kPad;
   if (row_ok) {
     T.acode[q] = (uint8_t)acode;
-    T.araw[q] = real_row ? araw[rho] : (uint8_t)0;
+    T.araw[q] = ra;
   }
   const uint32_t *sbase = ck + (uint64_t)strip * CL.strip_words;
   int32_t Ho = -OPEN, E = kNeg16, hoUpPrevT = -OPEN, FbotT = kNeg16;
@@ -968,8 +996,8 @@ k_tb(KArgs A, int stage, int cls) {
     const int m = (int)p.a_len, n = (int)p.b_len;
     const CkLayout CL = ck_layout(R, st->box_n);   // layout of the forward pass's checkpoints
     const uint32_t *ck = reinterpret_cast<const uint32_t *>(A.pool + st->code_off);
-    const uint8_t *acodes = A.codes + p.a_off, *bcodes = A.codes + p.b_off;
     const uint8_t *araw = A.raw + p.a_off, *braw = A.raw + p.b_off;
+    const RawView acodes{araw, A.lut}, bcodes{braw, A.lut};
     const int i_end = st->i_end;
     int j_end = st->j_end;
     int cs = -1, cg = -1, cw = -1, trow0 = 0, tcmin = 0, tqmax = -1;

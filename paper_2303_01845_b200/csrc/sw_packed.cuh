@@ -50,8 +50,8 @@ __device__ __forceinline__ uint32_t vmax2u(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t splat16(uint32_t v) { return (v & 0xFFFFu) * 0x10001u; }
 
 // u8 profile (s - lo) for rows row0+lane*R .. +R-1 of one pair; PAD -> 0.
-template <int R>
-__device__ __forceinline__ void build_profile_u8(uint8_t *prof, const int8_t *mat, const View &rows,
+template <int R, typename V>
+__device__ __forceinline__ void build_profile_u8(uint8_t *prof, const int8_t *mat, const V &rows,
                                                  int m, int row0, int lane, int lo) {
   constexpr int P0 = prof_p0(R), P1 = prof_p1(R);
   int arow[R];
@@ -154,7 +154,7 @@ struct PackedLane {
 struct PackedPair {        // one of the two pairs a warp carries
   int64_t k;               // pair index (-1: none)
   int m, n;
-  View rows, cols;
+  RawView rows, cols;
   uint32_t *ck;            // checkpoint region (nullptr: no room -> box path)
   unsigned long long ck_off;
 };
@@ -188,25 +188,30 @@ k_score_packed(KArgs A, int stage, int cls) {
     const uint32_t cnt = *(volatile uint32_t *)&A.ctrs[stage * kNumClasses + cls];
     if (pos >= cnt) break;
     PackedPair P[2];
+    uint64_t arena_end = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t idx = pos + h;
       P[h].k = idx < cnt ? (int64_t)list_of(A, stage, cls)[idx] : -1;
       if (P[h].k >= 0) {
         const sw_pair_t p = A.pairs[P[h].k];
+        arena_end = max(arena_end, max(p.a_off + p.a_len, p.b_off + p.b_len));
         P[h].m = (int)p.a_len;
         P[h].n = (int)p.b_len;
-        P[h].rows = View{A.codes + p.a_off, 1};
-        P[h].cols = View{A.codes + p.b_off, 1};
+        const uint8_t *seq = A.ready ? A.raw : A.codes;
+        const uint8_t *lut = A.ready ? A.lut : nullptr;
+        P[h].rows = RawView{seq + p.a_off, lut};
+        P[h].cols = RawView{seq + p.b_off, lut};
       } else {
         P[h].m = 0;
         P[h].n = 0;
-        P[h].rows = View{A.codes, 1};
-        P[h].cols = View{A.codes, 1};
+        P[h].rows = RawView{A.codes, nullptr};
+        P[h].cols = RawView{A.codes, nullptr};
       }
       P[h].ck = nullptr;
       P[h].ck_off = 0;
     }
+    wait_arena(A, arena_end, lane);   // host-pipelined arena: its slices may still be arriving
     const int m = max(P[0].m, P[1].m), n = max(P[0].n, P[1].n);
     const int nstrips = (m + 32 * R - 1) / (32 * R);
     const CkLayout CL = ck_layout(R, n);

@@ -290,3 +290,30 @@ print(json.dumps({"bad": bad, "launches": launches}))
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["bad"] == [0, 0], res
     assert res["launches"][0] > 60, res      # several packed rounds ran
+
+
+def test_pipelined_host_upload_matches_resident_arena():
+    """sw_align_batch uploads the arena in slices while the packed forward
+    runs (each warp waits for its pairs' slices).  With a multi-slice arena and
+    the pair table shuffled against arena order -- early work waits on late
+    slices -- the host path must equal the device path on a resident arena."""
+    import torch
+    sa, sb = workloads.config3_bulk(30_000, seed=5)
+    arena, table = pack_codes(sa, sb)
+    assert arena.size > 12 << 20          # several 4 MiB slices
+    table = table[np.random.default_rng(3).permutation(len(table))]
+    p = _native.make_params(11, 1, matrix("blosum62"))
+    host, _ = _native.align_host(arena, table, p)
+    d_arena = torch.from_numpy(arena).cuda()
+    d_pairs = torch.from_numpy(table.view(np.uint8).copy()).cuda()
+    d_out = torch.empty(len(table) * 32, dtype=torch.uint8, device="cuda")
+    _native.align_device(d_arena.data_ptr(), arena.size, d_pairs.data_ptr(), len(table), p,
+                         d_out.data_ptr(), stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    dev = d_out.cpu().numpy().view(_native.RESULT_DTYPE)
+    for f in FIELDS + ("status",):
+        assert (host[f] == dev[f]).all(), f
+    pick = np.random.default_rng(2).choice(len(table), 300, replace=False)
+    ref = oracle.align_batch_c(arena, table[pick], 11, 1, matrix("blosum62"), threads=16)
+    got = np.stack([host[f][pick] for f in FIELDS], axis=1)
+    assert (got == ref[:, :7]).all()
