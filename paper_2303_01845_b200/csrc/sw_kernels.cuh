@@ -793,13 +793,18 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int R, int BPL
 // warp-uniform and compares loaded values exactly as the reference does.
 // ---------------------------------------------------------------------------
 constexpr int kTbWarps = 4;
-constexpr int kTbX = 42;      // tile columns: halo + 32 + G - 1 (<= 40) -> padded
 constexpr int16_t kNeg16 = -16384;  // boundary "-inf": below -open - ext for open <= 16383
 
+// Tile of class R: rows = G*R replayed + 1 halo, columns = G + 32 (halo +
+// 32 columns of the first forward lane + G - 1 skew), G = 32 / R.
+template <int R>
 struct TbSmem {
-  int16_t H[33][kTbX], E[33][kTbX], F[33][kTbX];  // row 0 / col 0 = halo
+  static constexpr int G = 32 / R;
+  static constexpr int kRows = G * R + 1;
+  static constexpr int kX = (G + 32 + 1) / 2 * 2;
+  int16_t H[kRows][kX], E[kRows][kX], F[kRows][kX];  // row 0 / col 0 = halo
   uint4 row[32];        // per tile row: (Ho, E) and (diag above, F_bot) at c_lo - 1, matrix row
-  uint8_t bcode[kTbX], braw[kTbX];
+  uint8_t bcode[kX], braw[kX];
   uint8_t acode[32], araw[32];
 };
 
@@ -808,7 +813,7 @@ __device__ __forceinline__ int32_t ulo(uint32_t x, int32_t B) { return (int32_t)
 __device__ __forceinline__ int32_t uhi(uint32_t x, int32_t B) { return (int32_t)(x >> 16) - B; }
 
 template <int R>
-__device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const uint32_t *ck,
+__device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, const uint32_t *ck,
                                           const CkLayout &CL, int strip, int g, int w, int m,
                                           int n, const RawView &acodes, const RawView &bcodes,
                                           const uint8_t *araw, const uint8_t *braw, int lane,
@@ -975,10 +980,10 @@ __device__ __forceinline__ void tb_replay(TbSmem &T, const int8_t *smat, const u
 }
 
 template <int R>
-__global__ void __launch_bounds__(kTbWarps * 32)
+__global__ void __launch_bounds__(kTbWarps * 32, (R >= 8 ? 7 : 6))
 k_tb(KArgs A, int stage, int cls) {
   struct Shared {
-    TbSmem t[kTbWarps];
+    TbSmem<R> t[kTbWarps];
     int8_t mat[kCodes * kCodes];
   };
   __shared__ __align__(16) Shared sh;   // one shared window base for tiles and matrix
@@ -986,7 +991,7 @@ k_tb(KArgs A, int stage, int cls) {
   for (int i = threadIdx.x; i < kCodes * kCodes; i += blockDim.x) smat[i] = A.mat[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  TbSmem &T = sh.t[warp];
+  TbSmem<R> &T = sh.t[warp];
   const int32_t OPEN = A.open_, EXT = A.ext, Bias = A.bias16;
   for (;;) {
     const int64_t k = next_item(A, stage, cls, lane);
