@@ -979,6 +979,149 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   __syncwarp();
 }
 
+// Traceback of one pair whose packed forward pass wrote checkpoints
+// (PairState: best, i_end, code_off, box_n, flags & kFlagNeedJ); one warp.
+template <int R>
+__device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8_t *smat,
+                                        int64_t k, int lane) {
+  const int32_t OPEN = A.open_, EXT = A.ext, Bias = A.bias16;
+  const sw_pair_t p = A.pairs[k];
+  PairState *st = A.st + k;
+  const int m = (int)p.a_len, n = (int)p.b_len;
+  const CkLayout CL = ck_layout(R, st->box_n);   // layout of the forward pass's checkpoints
+  const uint32_t *ck = reinterpret_cast<const uint32_t *>(A.pool + st->code_off);
+  const uint8_t *araw = A.raw + p.a_off, *braw = A.raw + p.b_off;
+  const RawView acodes{araw, A.lut}, bcodes{braw, A.lut};
+  const int i_end = st->i_end;
+  int j_end = st->j_end;
+  int cs = -1, cg = -1, cw = -1, trow0 = 0, tcmin = 0, tqmax = -1;
+  if (st->flags & kFlagNeedJ) {
+    // The packed forward pass knows best and i_end only.  j_end = first
+    // column of row i_end with H == best: the per-window running row maxima
+    // in the checkpoints give its window w*; replaying that tile gives the
+    // column (align.py:124 row-major-first end cell).
+    const int best = st->best;
+    const int strip = i_end / (32 * R);
+    const int t = (i_end - strip * 32 * R) / R, r = i_end - strip * 32 * R - t * R;
+    const uint32_t *rmcol = ck + (uint64_t)strip * CL.strip_words + 32ull * (R + 1 + r) + t;
+    int wstar = CL.nwin - 1;
+    for (int w0 = 1; w0 < CL.nwin; w0 += 32) {
+      const int w = w0 + lane;
+      bool hit = false;
+      if (w < CL.nwin) hit = (int32_t)(rmcol[(uint64_t)w * 32 * (2 * R + 1)] & 0xFFFFu) - Bias >= best;
+      const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+      if (hm) { wstar = w0 + __ffs(hm) - 1 - 1; break; }
+    }
+    const int g = t / CL.G;
+    const int kap_hi = min(32 * wstar - t + 31, n - 1);
+    tb_replay<R>(T, smat, ck, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+                 EXT, Bias, trow0, tcmin, i_end, kap_hi);
+    cs = strip; cg = g; cw = wstar;
+    const int q = i_end - trow0;
+    tqmax = q;
+    const int c = 32 * wstar - t + lane;
+    const bool hit = (c >= 0) && (c <= kap_hi) && ((int32_t)T.H[q + 1][c - tcmin + 1] >= best);
+    const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+    j_end = hm ? 32 * wstar - t + __ffs(hm) - 1 : -1;
+  }
+  int i = i_end + 1, j = j_end + 1, state = 0, matches = 0, aln = 0;
+  bool lost = j_end < 0;
+  for (;;) {
+    if (lost) break;
+    if (i == 0 || j == 0) {
+      lost = state != 0;
+      break;
+    }
+    const int rho = i - 1, kap = j - 1;
+    // fast path: still inside the replayed part of the current tile
+    int q = rho - trow0;
+    const int u = kap - (cw * 32 - (cg * CL.G + q / R));
+    if (!(cs >= 0 && q >= 0 && q <= tqmax && u >= 0 && u < 32)) {
+      const int strip = rho / (32 * R);
+      const int t = (rho - strip * 32 * R) / R;
+      const int g = t / CL.G;
+      const int w = (kap + t) >> 5;
+      tb_replay<R>(T, smat, ck, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+                   EXT, Bias, trow0, tcmin, rho, kap);
+      cs = strip; cg = g; cw = w;
+      q = rho - trow0;
+      tqmax = q;
+    }
+    const int x = kap - tcmin + 1;
+    // first tile column of tile row qq (its left halo is at x_first - 1)
+    const int t0 = cg * CL.G, tspan = min(t0 + CL.G, 32) - 1 - t0;
+    if (state == 0) {                       // align.py:137-151
+      // Resolve a diagonal run 32 cells at a time: lane k checks cell
+      // (q-k, x-k); the run continues while each cell is an H-state diagonal
+      // move (h != 0 and h == H[diag] + s) inside the replayed tile.
+      const int qq = q - lane, xx = x - lane;
+      bool ok = (qq >= 0) && (kap - lane >= 0);
+      ok = ok && (xx >= tspan - qq / R + 1);
+      bool dg = false, mt = false;
+      if (ok) {
+        const int32_t hk = T.H[qq + 1][xx];
+        const int32_t sk = smat[T.acode[qq] * kCodes + T.bcode[xx - 1]];
+        dg = (hk != 0) && (hk == (int32_t)T.H[qq][xx - 1] + sk);
+        mt = T.araw[qq] == T.braw[xx - 1];
+      }
+      const uint32_t run_mask = __ballot_sync(0xffffffffu, dg);
+      const uint32_t mt_mask = __ballot_sync(0xffffffffu, mt);
+      const int run = (run_mask == 0xffffffffu) ? 32 : __ffs(~run_mask) - 1;
+      if (run > 0) {
+        const uint32_t sel = run == 32 ? 0xffffffffu : ((1u << run) - 1u);
+        matches += __popc(mt_mask & sel);
+        aln += run; i -= run; j -= run;
+        continue;
+      }
+      const int32_t h = T.H[q + 1][x];
+      if (h == 0) break;
+      if (h == (int32_t)T.F[q + 1][x]) {
+        state = 1;
+      } else if (h == (int32_t)T.E[q + 1][x]) {
+        state = 2;
+      } else {
+        lost = true;
+        break;
+      }
+    } else if (state == 1) {                // align.py:152-160: vertical gap run
+      const int qq = q - lane;
+      const bool ok = (qq >= 0) && (x >= tspan - qq / R + 1);
+      const bool close =
+          ok && ((int32_t)T.F[qq + 1][x] == (int32_t)T.H[qq][x] - OPEN);
+      const uint32_t cm = __ballot_sync(0xffffffffu, close);
+      const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+      const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
+      int steps;
+      if (cm) { steps = __ffs(cm); state = 0; }
+      else steps = nvalid;
+      aln += steps; i -= steps;
+    } else {                                // align.py:161-169: horizontal gap run
+      const int xx = x - lane;
+      const bool ok = (kap - lane >= 0) && (xx >= tspan - q / R + 1);
+      const bool close =
+          ok && ((int32_t)T.E[q + 1][xx] == (int32_t)T.H[q + 1][xx - 1] - OPEN);
+      const uint32_t cm = __ballot_sync(0xffffffffu, close);
+      const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+      const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
+      int steps;
+      if (cm) { steps = __ffs(cm); state = 0; }
+      else steps = nvalid;
+      aln += steps; j -= steps;
+    }
+  }
+  if (lane == 0) {
+    sw_result_t r;
+    r.score = st->best;
+    r.i_begin = i; r.i_end = i_end;
+    r.j_begin = j; r.j_end = j_end;
+    r.matches = matches; r.aln_len = aln;
+    r.status = lost ? SW_STATUS_INTERNAL : SW_STATUS_OK;
+    A.out[k] = r;
+    st->j_end = j_end;
+    st->flags |= kFlagDone;
+  }
+}
+
 template <int R>
 __global__ void __launch_bounds__(kTbWarps * 32, (R >= 8 ? 7 : 6))
 k_tb(KArgs A, int stage, int cls) {
@@ -992,145 +1135,10 @@ k_tb(KArgs A, int stage, int cls) {
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   TbSmem<R> &T = sh.t[warp];
-  const int32_t OPEN = A.open_, EXT = A.ext, Bias = A.bias16;
   for (;;) {
     const int64_t k = next_item(A, stage, cls, lane);
     if (k < 0) break;
-    const sw_pair_t p = A.pairs[k];
-    PairState *st = A.st + k;
-    const int m = (int)p.a_len, n = (int)p.b_len;
-    const CkLayout CL = ck_layout(R, st->box_n);   // layout of the forward pass's checkpoints
-    const uint32_t *ck = reinterpret_cast<const uint32_t *>(A.pool + st->code_off);
-    const uint8_t *araw = A.raw + p.a_off, *braw = A.raw + p.b_off;
-    const RawView acodes{araw, A.lut}, bcodes{braw, A.lut};
-    const int i_end = st->i_end;
-    int j_end = st->j_end;
-    int cs = -1, cg = -1, cw = -1, trow0 = 0, tcmin = 0, tqmax = -1;
-    if (st->flags & kFlagNeedJ) {
-      // The packed forward pass knows best and i_end only.  j_end = first
-      // column of row i_end with H == best: the per-window running row maxima
-      // in the checkpoints give its window w*; replaying that tile gives the
-      // column (align.py:124 row-major-first end cell).
-      const int best = st->best;
-      const int strip = i_end / (32 * R);
-      const int t = (i_end - strip * 32 * R) / R, r = i_end - strip * 32 * R - t * R;
-      const uint32_t *rmcol = ck + (uint64_t)strip * CL.strip_words + 32ull * (R + 1 + r) + t;
-      int wstar = CL.nwin - 1;
-      for (int w0 = 1; w0 < CL.nwin; w0 += 32) {
-        const int w = w0 + lane;
-        bool hit = false;
-        if (w < CL.nwin) hit = (int32_t)(rmcol[(uint64_t)w * 32 * (2 * R + 1)] & 0xFFFFu) - Bias >= best;
-        const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-        if (hm) { wstar = w0 + __ffs(hm) - 1 - 1; break; }
-      }
-      const int g = t / CL.G;
-      const int kap_hi = min(32 * wstar - t + 31, n - 1);
-      tb_replay<R>(T, smat, ck, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
-                   EXT, Bias, trow0, tcmin, i_end, kap_hi);
-      cs = strip; cg = g; cw = wstar;
-      const int q = i_end - trow0;
-      tqmax = q;
-      const int c = 32 * wstar - t + lane;
-      const bool hit = (c >= 0) && (c <= kap_hi) && ((int32_t)T.H[q + 1][c - tcmin + 1] >= best);
-      const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-      j_end = hm ? 32 * wstar - t + __ffs(hm) - 1 : -1;
-    }
-    int i = i_end + 1, j = j_end + 1, state = 0, matches = 0, aln = 0;
-    bool lost = j_end < 0;
-    for (;;) {
-      if (lost) break;
-      if (i == 0 || j == 0) {
-        lost = state != 0;
-        break;
-      }
-      const int rho = i - 1, kap = j - 1;
-      // fast path: still inside the replayed part of the current tile
-      int q = rho - trow0;
-      const int u = kap - (cw * 32 - (cg * CL.G + q / R));
-      if (!(cs >= 0 && q >= 0 && q <= tqmax && u >= 0 && u < 32)) {
-        const int strip = rho / (32 * R);
-        const int t = (rho - strip * 32 * R) / R;
-        const int g = t / CL.G;
-        const int w = (kap + t) >> 5;
-        tb_replay<R>(T, smat, ck, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
-                     EXT, Bias, trow0, tcmin, rho, kap);
-        cs = strip; cg = g; cw = w;
-        q = rho - trow0;
-        tqmax = q;
-      }
-      const int x = kap - tcmin + 1;
-      // first tile column of tile row qq (its left halo is at x_first - 1)
-      const int t0 = cg * CL.G, tspan = min(t0 + CL.G, 32) - 1 - t0;
-      if (state == 0) {                       // align.py:137-151
-        // Resolve a diagonal run 32 cells at a time: lane k checks cell
-        // (q-k, x-k); the run continues while each cell is an H-state diagonal
-        // move (h != 0 and h == H[diag] + s) inside the replayed tile.
-        const int qq = q - lane, xx = x - lane;
-        bool ok = (qq >= 0) && (kap - lane >= 0);
-        ok = ok && (xx >= tspan - qq / R + 1);
-        bool dg = false, mt = false;
-        if (ok) {
-          const int32_t hk = T.H[qq + 1][xx];
-          const int32_t sk = smat[T.acode[qq] * kCodes + T.bcode[xx - 1]];
-          dg = (hk != 0) && (hk == (int32_t)T.H[qq][xx - 1] + sk);
-          mt = T.araw[qq] == T.braw[xx - 1];
-        }
-        const uint32_t run_mask = __ballot_sync(0xffffffffu, dg);
-        const uint32_t mt_mask = __ballot_sync(0xffffffffu, mt);
-        const int run = (run_mask == 0xffffffffu) ? 32 : __ffs(~run_mask) - 1;
-        if (run > 0) {
-          const uint32_t sel = run == 32 ? 0xffffffffu : ((1u << run) - 1u);
-          matches += __popc(mt_mask & sel);
-          aln += run; i -= run; j -= run;
-          continue;
-        }
-        const int32_t h = T.H[q + 1][x];
-        if (h == 0) break;
-        if (h == (int32_t)T.F[q + 1][x]) {
-          state = 1;
-        } else if (h == (int32_t)T.E[q + 1][x]) {
-          state = 2;
-        } else {
-          lost = true;
-          break;
-        }
-      } else if (state == 1) {                // align.py:152-160: vertical gap run
-        const int qq = q - lane;
-        const bool ok = (qq >= 0) && (x >= tspan - qq / R + 1);
-        const bool close =
-            ok && ((int32_t)T.F[qq + 1][x] == (int32_t)T.H[qq][x] - OPEN);
-        const uint32_t cm = __ballot_sync(0xffffffffu, close);
-        const uint32_t vm = __ballot_sync(0xffffffffu, ok);
-        const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
-        int steps;
-        if (cm) { steps = __ffs(cm); state = 0; }
-        else steps = nvalid;
-        aln += steps; i -= steps;
-      } else {                                // align.py:161-169: horizontal gap run
-        const int xx = x - lane;
-        const bool ok = (kap - lane >= 0) && (xx >= tspan - q / R + 1);
-        const bool close =
-            ok && ((int32_t)T.E[q + 1][xx] == (int32_t)T.H[q + 1][xx - 1] - OPEN);
-        const uint32_t cm = __ballot_sync(0xffffffffu, close);
-        const uint32_t vm = __ballot_sync(0xffffffffu, ok);
-        const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
-        int steps;
-        if (cm) { steps = __ffs(cm); state = 0; }
-        else steps = nvalid;
-        aln += steps; j -= steps;
-      }
-    }
-    if (lane == 0) {
-      sw_result_t r;
-      r.score = st->best;
-      r.i_begin = i; r.i_end = i_end;
-      r.j_begin = j; r.j_end = j_end;
-      r.matches = matches; r.aln_len = aln;
-      r.status = lost ? SW_STATUS_INTERNAL : SW_STATUS_OK;
-      A.out[k] = r;
-      st->j_end = j_end;
-      st->flags |= kFlagDone;
-    }
+    tb_pair<R>(A, T, smat, k, lane);
   }
 }
 
