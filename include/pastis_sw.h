@@ -46,6 +46,7 @@ extern "C" {
 #define SW_EINVAL (-1)   /* bad arguments / parameters outside the supported domain */
 #define SW_ECUDA (-2)    /* CUDA runtime error (no device, OOM, launch failure) */
 #define SW_EINTERNAL (-3)
+#define SW_EFORMAT (-4)  /* malformed input text (sw_fasta_parse: see info->error) */
 
 /* per-pair status codes (sw_result_t.status) */
 #define SW_STATUS_OK 0
@@ -144,6 +145,40 @@ void sw_release(int device);
  * Returns NULL on failure (sw_last_error). */
 void *sw_host_alloc(uint64_t bytes);
 void sw_host_free(void *p);
+
+/* ---- FASTA ingest (the input side of the path) -----------
+ * sw_fasta_parse replaces seqio.read_fasta (seqio.py:42-92) for ASCII text:
+ * records in file order; residues concatenated, stripped, upper-cased, bytes
+ * outside the alphabet mapped to 'X' (counted in n_mapped: seqio.py:88-89);
+ * header = first whitespace-delimited token of the '>' line.  The residues
+ * land directly in `arena` (the byte arena sw_align_batch consumes), the
+ * header tokens in `headers`.  Capacities: arena and headers >= text_bytes,
+ * recs_cap >= number of '>' bytes in the text.  Returns SW_OK, SW_EINVAL
+ * (bad arguments / recs_cap too small) or SW_EFORMAT with info->error set to
+ * the reference's first error (FastaError, seqio.py:19) or SW_FASTA_NONASCII
+ * (Unicode text: the caller applies Python's str semantics itself). */
+#define SW_FASTA_NONASCII 1            /* input has bytes >= 0x80 */
+#define SW_FASTA_DATA_BEFORE_HEADER 2  /* "residue data before first header" (seqio.py:82-83) */
+#define SW_FASTA_EMPTY_HEADER 3        /* "record with empty description line" (seqio.py:78-79) */
+#define SW_FASTA_EMPTY_SEQ 4           /* "record ... has an empty sequence" (seqio.py:66-67) */
+#define SW_FASTA_NO_RECORDS 5          /* "no FASTA records" (seqio.py:86-87) */
+
+typedef struct sw_fasta_rec_t {
+  uint64_t off;       /* residues: arena[off, off + len) */
+  uint64_t hdr_off;   /* header token: headers[hdr_off, hdr_off + hdr_len) */
+  uint32_t len;
+  uint32_t hdr_len;
+} sw_fasta_rec_t;     /* 24 bytes */
+
+typedef struct sw_fasta_info_t {
+  uint64_t n_recs, arena_bytes, header_bytes, n_mapped;
+  int32_t error;      /* 0 or SW_FASTA_* */
+  uint32_t error_hdr_len;
+  uint64_t error_hdr_off;   /* SW_FASTA_EMPTY_SEQ: the record's header in `headers` */
+} sw_fasta_info_t;
+
+int sw_fasta_parse(const uint8_t *text, uint64_t text_bytes, uint8_t *arena, uint8_t *headers,
+                   sw_fasta_rec_t *recs, uint64_t recs_cap, sw_fasta_info_t *info);
 
 #ifdef __cplusplus
 }

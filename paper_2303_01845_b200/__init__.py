@@ -20,6 +20,7 @@ from .align import (
 )
 from .batch import PackedBatch, pack_pairs
 from .edges import SimilarityEdge, canonical_bytes, evaluate_records, format_edge_line
+from .seqio import FastaArena, FastaError, SequenceRecord, arena_pairs, read_fasta, read_fasta_arena
 
 __version__ = "0.1.0"
 
@@ -29,15 +30,21 @@ __all__ = [
     "AlignmentError",
     "AlignmentResult",
     "BatchCounters",
+    "FastaArena",
+    "FastaError",
     "PackedBatch",
+    "SequenceRecord",
     "SimilarityEdge",
     "align_batch",
     "align_packed",
+    "arena_pairs",
     "canonical_bytes",
     "encode",
     "evaluate_pair",
     "evaluate_records",
     "format_edge_line",
     "pack_pairs",
+    "read_fasta",
+    "read_fasta_arena",
     "smith_waterman",
 ]

@@ -31,7 +31,7 @@ RESULT_DTYPE = np.dtype(
 )
 assert PAIR_DTYPE.itemsize == 24 and RESULT_DTYPE.itemsize == 32
 
-SW_OK, SW_EINVAL, SW_ECUDA, SW_EINTERNAL = 0, -1, -2, -3
+SW_OK, SW_EINVAL, SW_ECUDA, SW_EINTERNAL, SW_EFORMAT = 0, -1, -2, -3, -4
 STATUS_OK, STATUS_EMPTY, STATUS_INTERNAL = 0, 1, 2
 
 # every symbol include/pastis_sw.h declares
@@ -46,7 +46,13 @@ EXPORTED_SYMBOLS = (
     "sw_release",
     "sw_host_alloc",
     "sw_host_free",
+    "sw_fasta_parse",
 )
+
+# FASTA ingest (sw_fasta_parse)
+FASTA_REC_DTYPE = np.dtype([("off", "<u8"), ("hdr_off", "<u8"), ("len", "<u4"), ("hdr_len", "<u4")])
+assert FASTA_REC_DTYPE.itemsize == 24
+FASTA_NONASCII, FASTA_DATA_BEFORE_HEADER, FASTA_EMPTY_HEADER, FASTA_EMPTY_SEQ, FASTA_NO_RECORDS = 1, 2, 3, 4, 5
 
 
 class SwParams(ctypes.Structure):
@@ -76,6 +82,13 @@ class SwTiming(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class SwFastaInfo(ctypes.Structure):
+    _fields_ = [("n_recs", ctypes.c_uint64), ("arena_bytes", ctypes.c_uint64),
+                ("header_bytes", ctypes.c_uint64), ("n_mapped", ctypes.c_uint64),
+                ("error", ctypes.c_int32), ("error_hdr_len", ctypes.c_uint32),
+                ("error_hdr_off", ctypes.c_uint64)]
 
 
 class NativeError(RuntimeError):
@@ -122,6 +135,8 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
         lib.sw_host_alloc.argtypes = [u64]
         lib.sw_host_free.restype = None
         lib.sw_host_free.argtypes = [vp]
+        lib.sw_fasta_parse.restype = i32
+        lib.sw_fasta_parse.argtypes = [vp, u64, vp, vp, vp, u64, ctypes.POINTER(SwFastaInfo)]
         if path is None:
             _lib = lib
         return lib
@@ -202,3 +217,26 @@ def partition(pairs: np.ndarray, n_shards: int):
     _check(lib.sw_partition_pairs(_ptr(pairs), len(pairs), n_shards, _ptr(shard),
                                   load_.ctypes.data))
     return shard, load_
+
+
+def fasta_parse(text: bytes):
+    """sw_fasta_parse on a whole FASTA text (host only, no GPU needed).
+
+    Returns (arena uint8[arena_bytes], headers bytes, recs FASTA_REC_DTYPE[n],
+    info dict); info["error"] != 0 reports the reference's first FastaError
+    (or FASTA_NONASCII) -- the caller raises it."""
+    lib = load()
+    buf = np.frombuffer(text, dtype=np.uint8) if len(text) else np.zeros(1, np.uint8)
+    n = len(text)
+    arena = np.empty(max(n, 1), dtype=np.uint8)
+    headers = np.empty(max(n, 1), dtype=np.uint8)
+    cap = int(np.count_nonzero(buf[:n] == ord(">"))) + 1
+    recs = np.empty(cap, dtype=FASTA_REC_DTYPE)
+    info = SwFastaInfo()
+    rc = lib.sw_fasta_parse(_ptr(buf), n, _ptr(arena), _ptr(headers), _ptr(recs), cap,
+                            ctypes.byref(info))
+    if rc not in (SW_OK, SW_EFORMAT):
+        _check(rc)
+    d = {name: getattr(info, name) for name, _ in SwFastaInfo._fields_}
+    return (arena[: info.arena_bytes], headers[: info.header_bytes].tobytes(),
+            recs[: info.n_recs].copy(), d)

@@ -28,7 +28,7 @@ def _stale(target, sources):
 
 def build_native(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))
-            if f.endswith((".cu", ".cuh"))]
+            if f.endswith((".cu", ".cuh", ".h"))]
     srcs.append(os.path.join(ROOT, "include", "pastis_sw.h"))
     if force or _stale(LIB, srcs):
         cmd = [NVCC, *NVCC_FLAGS, "-o", LIB, os.path.join(CSRC, "sw_engine.cu")]

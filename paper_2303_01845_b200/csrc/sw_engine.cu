@@ -26,6 +26,7 @@
 #include "sw_kernels.cuh"
 #include "sw_packed.cuh"
 #include "sw_cta.cuh"
+#include "sw_fasta.h"
 
 using namespace pastis;
 
@@ -724,6 +725,16 @@ int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena
   for (int d = 0; d < n_devices; ++d)
     for (size_t q = 0; q < sh[d].idx.size(); ++q) out[sh[d].idx[q]] = sh[d].out[q];
   return SW_OK;
+}
+
+int sw_fasta_parse(const uint8_t *text, uint64_t text_bytes, uint8_t *arena, uint8_t *headers,
+                   sw_fasta_rec_t *recs, uint64_t recs_cap, sw_fasta_info_t *info) {
+  if (!info || (text_bytes && (!text || !arena || !headers || (!recs && recs_cap))))
+    return fail(SW_EINVAL, "sw_fasta_parse: NULL buffer");
+  const int rc = pastis_fasta::parse(text, text_bytes, arena, headers, recs, recs_cap, info);
+  if (rc == SW_EINVAL) return fail(SW_EINVAL, "sw_fasta_parse: recs_cap too small");
+  if (rc == SW_EFORMAT) return fail(SW_EFORMAT, "malformed FASTA text");
+  return rc;
 }
 
 void sw_release(int device) {
