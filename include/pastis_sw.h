@@ -47,6 +47,7 @@ extern "C" {
 #define SW_ECUDA (-2)    /* CUDA runtime error (no device, OOM, launch failure) */
 #define SW_EINTERNAL (-3)
 #define SW_EFORMAT (-4)  /* malformed input text (sw_fasta_parse: see info->error) */
+#define SW_ERANGE (-5)   /* output buffer too small (sw_kmer_candidates: see stats->performed) */
 
 /* per-pair status codes (sw_result_t.status) */
 #define SW_STATUS_OK 0
@@ -179,6 +180,43 @@ typedef struct sw_fasta_info_t {
 
 int sw_fasta_parse(const uint8_t *text, uint64_t text_bytes, uint8_t *arena, uint8_t *headers,
                    sw_fasta_rec_t *recs, uint64_t recs_cap, sw_fasta_info_t *info);
+
+/* ---- candidate discovery (the caller side of the path) ----
+ * sw_kmer_candidates replaces the reference's candidate stage: the overlap
+ * semiring product A*A^T of the sequence-by-k-mer matrix (kmer.py:56-126,
+ * sparse.local_spgemm sparse.py:236, blocked SUMMA summa.py, symmetry pruning
+ * balance.py:98-128) followed by the threshold/orientation filter
+ * (pipeline.py:290-303): every unordered pair i < j whose sequences share at
+ * least min_shared DISTINCT k-mers (k-mer code = base-25 over alphabet.py:8,
+ * first residue most significant, kmer.py:43-53; sequences shorter than k
+ * have none), sorted by (i, j), with its shared count.  Sequences are residue
+ * bytes in `arena` (seq_off/seq_len per sequence, e.g. from sw_fasta_parse).
+ * Requires ceil(log2(25^k)) + ceil(log2(n_seqs)) <= 64.  If out_cap is
+ * smaller than the number of candidates, returns SW_ERANGE with
+ * stats->performed set (call again with a larger buffer). */
+typedef struct sw_candidate_t {
+  uint32_t i, j;      /* i < j: a = rows = sequence i, b = columns = sequence j */
+  uint32_t count;     /* distinct shared k-mers (OverlapPayload.count, kmer.py:98) */
+  uint32_t pad;
+} sw_candidate_t;     /* 16 bytes */
+
+typedef struct sw_kmer_stats_t {
+  uint64_t positions;      /* k-mer occurrences */
+  uint64_t distinct;       /* nnz of A: distinct (sequence, k-mer) entries */
+  uint64_t buckets;        /* k-mers present in >= 1 sequence */
+  uint64_t emitted;        /* pair emissions = sum over k-mers of c(c-1)/2 */
+  uint64_t discovered;     /* unordered pairs sharing >= 1 k-mer (pruned overlap nnz) */
+  uint64_t performed;      /* candidates with count >= min_shared */
+  uint64_t flops;          /* semiring multiplies of A*A^T = sum over k-mers of c^2 */
+  uint32_t short_seqs;     /* sequences shorter than k (kmer.py:87-88) */
+  uint32_t pad;
+  double device_ms;
+} sw_kmer_stats_t;
+
+int sw_kmer_candidates(int device, const uint8_t *arena, uint64_t arena_bytes,
+                       const uint64_t *seq_off, const uint32_t *seq_len, uint32_t n_seqs, int k,
+                       uint32_t min_shared, sw_candidate_t *out, uint64_t out_cap,
+                       sw_kmer_stats_t *stats);
 
 #ifdef __cplusplus
 }

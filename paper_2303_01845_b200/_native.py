@@ -31,7 +31,7 @@ RESULT_DTYPE = np.dtype(
 )
 assert PAIR_DTYPE.itemsize == 24 and RESULT_DTYPE.itemsize == 32
 
-SW_OK, SW_EINVAL, SW_ECUDA, SW_EINTERNAL, SW_EFORMAT = 0, -1, -2, -3, -4
+SW_OK, SW_EINVAL, SW_ECUDA, SW_EINTERNAL, SW_EFORMAT, SW_ERANGE = 0, -1, -2, -3, -4, -5
 STATUS_OK, STATUS_EMPTY, STATUS_INTERNAL = 0, 1, 2
 
 # every symbol include/pastis_sw.h declares
@@ -47,7 +47,12 @@ EXPORTED_SYMBOLS = (
     "sw_host_alloc",
     "sw_host_free",
     "sw_fasta_parse",
+    "sw_kmer_candidates",
 )
+
+# candidate discovery (sw_kmer_candidates)
+CANDIDATE_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4"), ("count", "<u4"), ("pad", "<u4")])
+assert CANDIDATE_DTYPE.itemsize == 16
 
 # FASTA ingest (sw_fasta_parse)
 FASTA_REC_DTYPE = np.dtype([("off", "<u8"), ("hdr_off", "<u8"), ("len", "<u4"), ("hdr_len", "<u4")])
@@ -89,6 +94,14 @@ class SwFastaInfo(ctypes.Structure):
                 ("header_bytes", ctypes.c_uint64), ("n_mapped", ctypes.c_uint64),
                 ("error", ctypes.c_int32), ("error_hdr_len", ctypes.c_uint32),
                 ("error_hdr_off", ctypes.c_uint64)]
+
+
+class SwKmerStats(ctypes.Structure):
+    _fields_ = [("positions", ctypes.c_uint64), ("distinct", ctypes.c_uint64),
+                ("buckets", ctypes.c_uint64), ("emitted", ctypes.c_uint64),
+                ("discovered", ctypes.c_uint64), ("performed", ctypes.c_uint64),
+                ("flops", ctypes.c_uint64), ("short_seqs", ctypes.c_uint32),
+                ("pad", ctypes.c_uint32), ("device_ms", ctypes.c_double)]
 
 
 class NativeError(RuntimeError):
@@ -135,6 +148,9 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
         lib.sw_host_alloc.argtypes = [u64]
         lib.sw_host_free.restype = None
         lib.sw_host_free.argtypes = [vp]
+        lib.sw_kmer_candidates.restype = i32
+        lib.sw_kmer_candidates.argtypes = [i32, vp, u64, vp, vp, ctypes.c_uint32, i32,
+                                           ctypes.c_uint32, vp, u64, ctypes.POINTER(SwKmerStats)]
         lib.sw_fasta_parse.restype = i32
         lib.sw_fasta_parse.argtypes = [vp, u64, vp, vp, vp, u64, ctypes.POINTER(SwFastaInfo)]
         if path is None:
@@ -240,3 +256,24 @@ def fasta_parse(text: bytes):
     d = {name: getattr(info, name) for name, _ in SwFastaInfo._fields_}
     return (arena[: info.arena_bytes], headers[: info.header_bytes].tobytes(),
             recs[: info.n_recs].copy(), d)
+
+
+def kmer_candidates(arena: np.ndarray, offsets: np.ndarray, lengths: np.ndarray, k: int,
+                    min_shared: int, device: int = 0):
+    """sw_kmer_candidates: (candidates CANDIDATE_DTYPE sorted by (i, j), stats dict)."""
+    lib = load()
+    arena = np.ascontiguousarray(arena, dtype=np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    lengths = np.ascontiguousarray(lengths, dtype=np.uint32)
+    cap = max(1024, 4 * len(lengths))
+    while True:
+        out = np.empty(cap, dtype=CANDIDATE_DTYPE)
+        st = SwKmerStats()
+        rc = lib.sw_kmer_candidates(device, _ptr(arena), arena.size, _ptr(offsets), _ptr(lengths),
+                                    len(lengths), k, min_shared, _ptr(out), cap, ctypes.byref(st))
+        if rc == SW_ERANGE:
+            cap = int(st.performed)
+            continue
+        _check(rc)
+        d = {name: getattr(st, name) for name, _ in SwKmerStats._fields_ if name != "pad"}
+        return out[: st.performed], d

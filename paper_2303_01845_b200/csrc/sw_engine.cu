@@ -22,11 +22,17 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "sw_kernels.cuh"
 #include "sw_packed.cuh"
 #include "sw_cta.cuh"
 #include "sw_fasta.h"
+#include "sw_kmer.cuh"
 
 using namespace pastis;
 
@@ -83,6 +89,7 @@ struct DeviceCtx {
   std::mutex mu;
   DevBuf arena, codes, pairs, out, st, lists, ctrs, stats, mat, lut, bnd, pool;
   DevBuf skeys, svals, cubtmp;  // work-list sort
+  DevBuf km_arena, km_off, km_len, km_base, km_keys, km_runs, km_pairs, km_out, km_small;
   cudaEvent_t ev[16];
   // one stream per length class: the packed forward + tile traceback of each
   // class run concurrently so the tail of one class overlaps the others
@@ -592,6 +599,196 @@ int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_
   return SW_OK;
 }
 
+struct Square {
+  __host__ __device__ uint64_t operator()(uint32_t c) const { return (uint64_t)c * c; }
+};
+struct Widen {
+  __host__ __device__ uint64_t operator()(uint32_t c) const { return c; }
+};
+struct Flag {
+  uint32_t t;
+  __host__ __device__ uint64_t operator()(uint32_t c) const { return c >= t ? 1ull : 0ull; }
+};
+
+int bits_for(uint64_t v) {   // smallest b with v <= 2^b
+  int b = 0;
+  while (b < 64 && (1ull << b) < v) ++b;
+  return b;
+}
+
+template <typename F>
+int cub_call(DeviceCtx *c, F &&f) {   // two-phase CUB call with the shared temp buffer
+  size_t bytes = 0;
+  CU(f(nullptr, bytes));
+  CU(c->cubtmp.ensure(bytes + 16));
+  CU(f(c->cubtmp.p, bytes));
+  return SW_OK;
+}
+
+int kmer_candidates(int device, const uint8_t *arena, uint64_t arena_bytes, const uint64_t *seq_off,
+                    const uint32_t *seq_len, uint32_t n_seqs, int k, uint32_t min_shared,
+                    sw_candidate_t *out, uint64_t out_cap, sw_kmer_stats_t *st) {
+  if (!st) return fail(SW_EINVAL, "stats is NULL");
+  memset(st, 0, sizeof(*st));
+  if (k < 1) return fail(SW_EINVAL, "k must be >= 1");
+  if (n_seqs && (!seq_off || !seq_len)) return fail(SW_EINVAL, "NULL sequence table");
+  uint64_t space = 1;
+  for (int t = 0; t < k; ++t) {
+    if (space > (~0ull) / 25) return fail(SW_EINVAL, "25^k does not fit in 64 bits");
+    space *= 25;
+  }
+  const int code_bits = bits_for(space);
+  const int seq_bits = std::max(1, bits_for(n_seqs));
+  if (code_bits + seq_bits > 64 || 2 * seq_bits > 64)
+    return fail(SW_EINVAL, "k-mer code space and sequence count exceed 64-bit keys");
+  std::vector<uint64_t> base(n_seqs + 1, 0);
+  uint64_t P = 0;
+  for (uint32_t s = 0; s < n_seqs; ++s) {
+    if (seq_off[s] + seq_len[s] > arena_bytes) return fail(SW_EINVAL, "sequence outside the arena");
+    base[s] = P;
+    if (seq_len[s] >= (uint32_t)k) P += seq_len[s] - k + 1;
+    else ++st->short_seqs;
+  }
+  base[n_seqs] = P;
+  st->positions = P;
+  if (P > 0x7FFFFFF0ull) return fail(SW_EINVAL, "too many k-mer positions in one call");
+  DeviceCtx *c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(c->mu);
+  CU(cudaSetDevice(device));
+  cudaStream_t s = c->stream;
+  if (P == 0) {
+    st->performed = 0;
+    return SW_OK;
+  }
+  CU(cudaEventRecord(c->ev[0], s));
+  CU(c->km_arena.ensure(arena_bytes + 16));
+  CU(c->km_off.ensure(n_seqs * 8 + 8));
+  CU(c->km_len.ensure(n_seqs * 4 + 4));
+  CU(c->km_base.ensure((n_seqs + 1) * 8));
+  CU(c->km_keys.ensure(2 * P * 8));
+  CU(c->km_small.ensure(64));
+  CU(cudaMemcpyAsync(c->km_arena.p, arena, arena_bytes, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->km_off.p, seq_off, n_seqs * 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->km_len.p, seq_len, n_seqs * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->km_base.p, base.data(), (n_seqs + 1) * 8, cudaMemcpyHostToDevice, s));
+  uint64_t *keys_a = (uint64_t *)c->km_keys.p, *keys_b = keys_a + P;
+  // 1. keys of every occurrence
+  k_kmer_keys<<<(unsigned)std::min<uint64_t>((n_seqs + 7) / 8, (uint64_t)c->sms * 16), 256, 0, s>>>(
+      (const uint8_t *)c->km_arena.p, (const uint64_t *)c->km_off.p, (const uint32_t *)c->km_len.p,
+      (const uint64_t *)c->km_base.p, n_seqs, k, seq_bits, (const uint8_t *)c->lut.p, keys_a);
+  CU(cudaGetLastError());
+  // 2. sort + unique (code, seq)
+  const int key_bits = code_bits + seq_bits;
+  rc = cub_call(c, [&](void *t, size_t &b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, keys_a, keys_b, (int)P, 0, key_bits, s);
+  });
+  if (rc) return rc;
+  uint64_t *nsel = (uint64_t *)c->km_small.p;   // [0] unique, [1] runs, [2] pairs, [3] flops
+  rc = cub_call(c, [&](void *t, size_t &b) {
+    return cub::DeviceSelect::Unique(t, b, keys_b, keys_a, nsel, (int)P, s);
+  });
+  if (rc) return rc;
+  uint64_t U = 0;
+  CU(cudaMemcpyAsync(&U, nsel, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  st->distinct = U;
+  // 3. buckets = runs of equal code
+  CU(c->km_runs.ensure(U * (8 + 4 + 8 + 8) + 64));
+  uint64_t *run_code = (uint64_t *)c->km_runs.p;
+  uint32_t *run_cnt = (uint32_t *)(run_code + U);
+  uint64_t *run_start = (uint64_t *)(((uintptr_t)(run_cnt + U) + 15) & ~(uintptr_t)15);
+  uint64_t *run_emit = run_start + U;
+  auto codes_it = thrust::make_transform_iterator(keys_a, KeyShift{seq_bits});
+  rc = cub_call(c, [&](void *t, size_t &b) {
+    return cub::DeviceRunLengthEncode::Encode(t, b, codes_it, run_code, run_cnt, nsel + 1, (int)U, s);
+  });
+  if (rc) return rc;
+  uint64_t R = 0;
+  CU(cudaMemcpyAsync(&R, nsel + 1, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  st->buckets = R;
+  auto cnt_it = thrust::make_transform_iterator(run_cnt, Widen{});
+  auto emit_it = thrust::make_transform_iterator(run_cnt, PairsOf{});
+  auto sq_it = thrust::make_transform_iterator(run_cnt, Square{});
+  rc = cub_call(c, [&](void *t, size_t &b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, cnt_it, run_start, (int)R, s);
+  });
+  if (rc) return rc;
+  rc = cub_call(c, [&](void *t, size_t &b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, emit_it, run_emit, (int)R, s);
+  });
+  if (rc) return rc;
+  rc = cub_call(c, [&](void *t, size_t &b) {
+    return cub::DeviceReduce::Sum(t, b, sq_it, nsel + 3, (int)R, s);
+  });
+  if (rc) return rc;
+  uint64_t last_off = 0, flops = 0;
+  uint32_t last_cnt = 0;
+  CU(cudaMemcpyAsync(&last_off, run_emit + (R - 1), 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&last_cnt, run_cnt + (R - 1), 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&flops, nsel + 3, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const uint64_t E = last_off + (uint64_t)last_cnt * (last_cnt - 1) / 2;
+  st->emitted = E;
+  st->flops = flops;
+  if (E > 0x7FFFFFF0ull) return fail(SW_EINVAL, "too many shared-k-mer pair emissions in one call");
+  uint64_t D = 0, C = 0;
+  if (E > 0) {
+    // 4. pairs of every bucket
+    CU(c->km_pairs.ensure(2 * E * 8 + E * 4 + 64));
+    uint64_t *pairs_a = (uint64_t *)c->km_pairs.p, *pairs_b = pairs_a + E;
+    uint32_t *pcnt = (uint32_t *)(pairs_b + E);   // shared count per distinct pair
+    k_bucket_pairs<<<(unsigned)std::min<uint64_t>((R + 7) / 8, (uint64_t)c->sms * 16), 256, 0, s>>>(
+        keys_a, run_cnt, run_start, run_emit, R, seq_bits, pairs_a);
+    CU(cudaGetLastError());
+    // 5. sort pair keys, count runs
+    rc = cub_call(c, [&](void *t, size_t &b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, pairs_a, pairs_b, (int)E, 0, 2 * seq_bits, s);
+    });
+    if (rc) return rc;
+    // distinct pairs into pairs_a, their counts into pcnt
+    rc = cub_call(c, [&](void *t, size_t &b) {
+      return cub::DeviceRunLengthEncode::Encode(t, b, pairs_b, pairs_a, pcnt, nsel + 2, (int)E, s);
+    });
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(&D, nsel + 2, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    // threshold + order-preserving compaction
+    uint64_t *cursor = pairs_b;   // free now (E >= D)
+    auto flag_it = thrust::make_transform_iterator(pcnt, Flag{min_shared});
+    rc = cub_call(c, [&](void *t, size_t &b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, flag_it, cursor, (int)D, s);
+    });
+    if (rc) return rc;
+    uint64_t last_cur = 0;
+    uint32_t last_pc = 0;
+    CU(cudaMemcpyAsync(&last_cur, cursor + (D - 1), 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&last_pc, pcnt + (D - 1), 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    C = last_cur + (last_pc >= min_shared ? 1 : 0);
+    if (C > 0) {
+      CU(c->km_out.ensure(C * sizeof(sw_candidate_t)));
+      k_write_candidates<<<(unsigned)std::min<uint64_t>((D + 255) / 256, (uint64_t)c->sms * 16), 256,
+                           0, s>>>(pairs_a, pcnt, D, seq_bits, min_shared, cursor,
+                                   (sw_candidate_t *)c->km_out.p);
+      CU(cudaGetLastError());
+    }
+  }
+  CU(cudaEventRecord(c->ev[1], s));
+  CU(cudaStreamSynchronize(s));
+  st->discovered = D;
+  st->performed = C;
+  st->device_ms = ev_ms(c->ev[0], c->ev[1]);
+  if (C > out_cap) return fail(SW_ERANGE, "candidate buffer too small (see stats->performed)");
+  if (C > 0) {
+    if (!out) return fail(SW_EINVAL, "NULL candidate buffer");
+    CU(cudaMemcpy(out, c->km_out.p, C * sizeof(sw_candidate_t), cudaMemcpyDeviceToHost));
+  }
+  return SW_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -737,6 +934,14 @@ int sw_fasta_parse(const uint8_t *text, uint64_t text_bytes, uint8_t *arena, uin
   return rc;
 }
 
+int sw_kmer_candidates(int device, const uint8_t *arena, uint64_t arena_bytes,
+                       const uint64_t *seq_off, const uint32_t *seq_len, uint32_t n_seqs, int k,
+                       uint32_t min_shared, sw_candidate_t *out, uint64_t out_cap,
+                       sw_kmer_stats_t *stats) {
+  return kmer_candidates(device, arena, arena_bytes, seq_off, seq_len, n_seqs, k, min_shared, out,
+                         out_cap, stats);
+}
+
 void sw_release(int device) {
   std::lock_guard<std::mutex> g(g_ctx_mu);
   for (size_t d = 0; d < g_ctx.size(); ++d) {
@@ -746,7 +951,9 @@ void sw_release(int device) {
     std::lock_guard<std::mutex> g2(c->mu);
     cudaSetDevice((int)d);
     for (DevBuf *b : {&c->arena, &c->codes, &c->pairs, &c->out, &c->st, &c->lists, &c->ctrs,
-                      &c->stats, &c->bnd, &c->pool, &c->skeys, &c->svals, &c->cubtmp})
+                      &c->stats, &c->bnd, &c->pool, &c->skeys, &c->svals, &c->cubtmp,
+                      &c->km_arena, &c->km_off, &c->km_len, &c->km_base, &c->km_keys, &c->km_runs,
+                      &c->km_pairs, &c->km_out, &c->km_small})
       b->release();
     c->pool_want = 0;
   }
