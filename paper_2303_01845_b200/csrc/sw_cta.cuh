@@ -25,6 +25,7 @@ struct CtaSync {               // per-CTA shared state
   volatile int prod[kCtaWarps];   // columns published into the link leaving warp w
   volatile int cons[kCtaWarps];   // columns consumed from the link leaving warp w
   int64_t item;
+  volatile int dead_strip;      // reverse pass: first strip whose bottom row carries no live path
   unsigned long long red_fwd[kCtaWarps];
   int red_x[kCtaWarps], red_y[kCtaWarps], red_v[kCtaWarps];
 };
@@ -41,13 +42,18 @@ k_score_cta(KArgs A, int stage, int cls) {
   load_matrix(smat, A.mat);
   int2 *wrap = A.bnd + (uint64_t)blockIdx.x * A.bnd_stride;   // warp W-1 -> warp 0 row
   const int32_t OPEN = A.open_ << 16, nEXT = -(A.ext << 16);
-  const int2 dflt = make_int2(-OPEN, kNegInf);
+  // reverse pass (MODE 1): anchored at the end cell, floored, stopped after a
+  // round of strips whose bottom row is dead -- see score_pair (sw_kernels.cuh)
+  const int32_t FLOOR = (int32_t)max(-32600, -32766 + A.open_ + A.ext) * 65536;
+  const int32_t ANC = FLOOR - OPEN;
+  const int2 dflt = MODE == 1 ? make_int2(ANC, ANC) : make_int2(-OPEN, kNegInf);
   for (;;) {
     if (threadIdx.x == 0) {
       const uint32_t pos = atomicAdd(&A.ctrs[kStages * kNumClasses + stage * kNumClasses + cls], 1u);
       const uint32_t cnt = *(volatile uint32_t *)&A.ctrs[stage * kNumClasses + cls];
       S.item = pos < cnt ? (int64_t)list_of(A, stage, cls)[pos] : -1;
       for (int w = 0; w < kCtaWarps; ++w) { S.prod[w] = 0; S.cons[w] = 0; }
+      S.dead_strip = 0x7fffffff;
     }
     __syncthreads();
     const int64_t k = S.item;
@@ -75,17 +81,30 @@ k_score_cta(KArgs A, int stage, int cls) {
     ScoreOut res{0ull, 0, 0, 0};
     const int in_link = (warp + kCtaWarps - 1) % kCtaWarps;   // link feeding this warp
     int prod_total = 0, cons_total = 0;   // this warp's counters on its out / in links
+    // reverse pass: once a strip is dead (S.dead_strip), every deeper strip
+    // is abandoned -- at its start, at each 32-column fetch and inside the
+    // ring waits; the dead strip itself has produced all its rows by then,
+    // so no producer is left waiting on an abandoned consumer
+    auto abandon = [&](int st) {
+      return MODE == 1 && __shfl_sync(0xffffffffu, (int)(S.dead_strip < st), 0) != 0;
+    };
     for (int strip = warp; strip < nstrips; strip += kCtaWarps) {
+      if (abandon(strip)) break;
       const int row0 = strip * 32 * R;
       __syncwarp();
       build_profile<R>(prof, smat, rows, m, row0, lane);
       __syncwarp();
       ScoreLane<R, false> L;
 #pragma unroll
-      for (int r = 0; r < R; ++r) { L.Ho[r] = -OPEN; L.E[r] = kNegInf; L.key[r] = 0; }
-      L.hoUpPrev = -OPEN;
-      L.botHo = -OPEN;
-      L.botF = kNegInf;
+      for (int r = 0; r < R; ++r) {
+        L.Ho[r] = MODE == 1 ? ANC : -OPEN;
+        L.E[r] = MODE == 1 ? ANC : kNegInf;
+        L.key[r] = 0;
+      }
+      L.hoUpPrev = (MODE == 1 && !(strip == 0 && lane == 0)) ? ANC : -OPEN;
+      L.botHo = MODE == 1 ? ANC : -OPEN;
+      L.botF = MODE == 1 ? ANC : kNegInf;
+      bool alive = false;
       L.code_next = lane == 0 ? cols.at(0) : kPad;
       const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
       const bool in_wrap = warp == 0;                  // fed by the global wrap row
@@ -99,7 +118,8 @@ k_score_cta(KArgs A, int stage, int cls) {
           const int need = min(s + kCtaChunk, n);
           if (s < n) {
             const int target = cons_total + (need - s);
-            while (S.prod[in_link] < target) __nanosleep(32);
+            while (S.prod[in_link] < target && !(MODE == 1 && S.dead_strip < strip)) __nanosleep(32);
+            if (abandon(strip)) break;
             __syncwarp();
             const int c = s + lane;
             cur = dflt;
@@ -134,7 +154,7 @@ k_score_cta(KArgs A, int stage, int cls) {
           const int32_t sc = (int32_t)prmt(word_of(pw, r), 0u, sel_scaled(r & 3));
           L.E[r] = __viaddmax_s32(L.E[r], nEXT, L.Ho[r]);
           const int32_t D = diag + sc + OPEN;
-          const int32_t t = __vimax_s32_relu(D, L.E[r]);
+          const int32_t t = MODE == 1 ? __vimax3_s32(D, L.E[r], FLOOR) : __vimax_s32_relu(D, L.E[r]);
           F = __viaddmax_s32(F, nEXT, hoUp);
           const int32_t h = max(t, F);
           diag = L.Ho[r];
@@ -150,12 +170,13 @@ k_score_cta(KArgs A, int stage, int cls) {
           if (cb >= 0 && cb < n) {
             if (!out_wrap && (cb % kCtaChunk) == 0) {      // flow control on the ring
               const int limit = prod_total + kCtaChunk - kRing;
-              while (S.cons[warp] < limit) __nanosleep(32);
+              while (S.cons[warp] < limit && !(MODE == 1 && S.dead_strip < strip)) __nanosleep(32);
             }
             if (lane == 31) {
               const int2 v = make_int2(L.botHo, L.botF);
               if (out_wrap) wrap[cb] = v;
               else ring_out[(prod_total) & (kRing - 1)] = v;
+              if (MODE == 1) alive |= (L.botHo > -OPEN) | (L.botF > -OPEN - nEXT);
             }
             ++prod_total;
             if ((prod_total & 7) == 0 || cb == n - 1) {
@@ -165,6 +186,8 @@ k_score_cta(KArgs A, int stage, int cls) {
           }
         }
       }
+      if (MODE == 1 && has_below && !__shfl_sync(0xffffffffu, (int)alive, 31) && lane == 0)
+        atomicMin((int *)&S.dead_strip, strip);
       // strip reduction (as k_score)
 #pragma unroll
       for (int r = 0; r < R; ++r) {

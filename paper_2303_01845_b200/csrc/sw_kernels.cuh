@@ -283,7 +283,7 @@ __device__ __forceinline__ void score_step(ScoreLane<R, WIDE> &L, const uint8_t 
                                            const int lane, const bool has_above,
                                            const bool has_below, BoundaryReader &br, int2 *bnd,
                                            const int2 dflt, const int32_t OPEN,
-                                           const int32_t nEXT) {
+                                           const int32_t nEXT, const int32_t FLOOR) {
   const int c = s - lane;
   const bool valid = (c >= 0) & (c < n);
   const int code = L.code_next;
@@ -298,7 +298,9 @@ __device__ __forceinline__ void score_step(ScoreLane<R, WIDE> &L, const uint8_t 
     const int2 b = br.get(bnd, s, n, lane, dflt);
     if (lane == 0) { upHo = b.x; upF = b.y; }
   } else if (lane == 0) {
-    upHo = -OPEN; upF = kNegInf;
+    // row 0: H = 0 (local) / -inf (anchored reverse pass, MODE 1)
+    upHo = MODE == 1 ? dflt.x : -OPEN;
+    upF = MODE == 1 ? dflt.y : kNegInf;
   }
   int32_t cc = 0;
   if (valid) cc = MODE == 0 ? 65535 - c : c + 1;
@@ -313,7 +315,8 @@ __device__ __forceinline__ void score_step(ScoreLane<R, WIDE> &L, const uint8_t 
     const int32_t sc = (int32_t)prmt(w, 0u, WIDE ? sel_plain(r & 3) : sel_scaled(r & 3));
     L.E[r] = __viaddmax_s32(L.E[r], nEXT, L.Ho[r]);
     const int32_t D = diag + sc + OPEN;
-    const int32_t t = __vimax_s32_relu(D, L.E[r]);
+    // forward: local (relu); reverse: anchored, floored at FLOOR (see score_pair)
+    const int32_t t = MODE == 1 ? __vimax3_s32(D, L.E[r], FLOOR) : __vimax_s32_relu(D, L.E[r]);
     F = __viaddmax_s32(F, nEXT, hoUp);
     const int32_t h = max(t, F);
     diag = L.Ho[r];
@@ -344,6 +347,22 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
   constexpr int SH = WIDE ? 0 : 16;
   const int32_t OPEN = open_ << SH;
   const int32_t nEXT = -(ext << SH);
+  // Reverse pass (MODE 1) = SW on the reversed prefixes ANCHORED at the end
+  // cell: only paths that start at reversed (0, 0) count (SURVEY App. A.6:
+  // same set of cells reaching best as the local version).  No 0-restarts:
+  // H = max(D, E, F, FLOOR), -inf boundaries except the anchor.  The floor
+  // keeps the scaled int32 intermediates from wrapping; it cannot change the
+  // set of cells == best (a restart at FLOOR reaches at most FLOOR + best <
+  // best); it sits 168 above the int32 limit of the scaled domain so that
+  // FLOOR - open - ext and FLOOR + s (s >= -128, the virtual cells) cannot
+  // wrap.  Every proper suffix of an optimal alignment scores > 0, so the
+  // optimal paths cross each row in H > 0 or, inside a gap, E/F > ext - open:
+  // once a strip's bottom row (all that feeds the strips below) has H <= 0
+  // and F <= ext - open everywhere, no later strip holds a cell == best and
+  // the pass stops.  Random long pairs die within a strip or two.
+  const int32_t FLOOR = WIDE ? -(1 << 28)
+                             : (int32_t)max(-32600, -32766 + open_ + ext) * 65536;
+  const int32_t ANC = FLOOR - OPEN;              // -inf in (H - open) form
   ScoreOut res{0ull, 0, 0, 0};
   const int nstrips = (m + 32 * R - 1) / (32 * R);
   for (int strip = 0; strip < nstrips; ++strip) {
@@ -353,14 +372,19 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
     __syncwarp();
     ScoreLane<R, WIDE> L;
 #pragma unroll
-    for (int r = 0; r < R; ++r) { L.Ho[r] = -OPEN; L.E[r] = kNegInf; L.key[r] = 0; }
-    L.hoUpPrev = -OPEN;
-    L.botHo = -OPEN;
-    L.botF = kNegInf;
+    for (int r = 0; r < R; ++r) {
+      L.Ho[r] = MODE == 1 ? ANC : -OPEN;
+      L.E[r] = MODE == 1 ? ANC : kNegInf;
+      L.key[r] = 0;
+    }
+    L.hoUpPrev = (MODE == 1 && !(strip == 0 && lane == 0)) ? ANC : -OPEN;   // anchor: H(0,0) = 0
+    L.botHo = MODE == 1 ? ANC : -OPEN;
+    L.botF = MODE == 1 ? ANC : kNegInf;
     L.code_next = lane == 0 ? cols.at(0) : kPad;
     const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
     BoundaryReader br;
-    const int2 dflt = make_int2(-OPEN, kNegInf);
+    const int2 dflt = MODE == 1 ? make_int2(ANC, ANC) : make_int2(-OPEN, kNegInf);
+    bool alive = false;   // MODE 1: does the strip's bottom row still carry a live path?
     if (has_above) br.init(bnd, n, lane, dflt);
     const int steps = n + 31;
     // checkpoints (forward pass of short/medium pairs): column checkpoints are
@@ -385,9 +409,13 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
 #pragma unroll 2
       for (int q = 0; q < kScoreUnroll; ++q) {
         score_step<R, MODE, WIDE>(L, prof, cols, s0 + q, n, lane, has_above, has_below, br, bnd,
-                                  dflt, OPEN, nEXT);
+                                  dflt, OPEN, nEXT, FLOOR);
         if constexpr (!WIDE && MODE == 0) {
           if (stage_slot) stage_slot[q] = pack_hi16(L.botHo, L.botF);
+        }
+        if constexpr (MODE == 1) {
+          const int cb = s0 + q - 31;   // lane 31's column (the strip's bottom row)
+          alive |= (cb >= 0) & (cb < n) & ((L.botHo > -OPEN) | (L.botF > -OPEN - nEXT));
         }
       }
       if constexpr (!WIDE && MODE == 0) {
@@ -427,6 +455,9 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
           res.rev_y = lo > res.rev_y ? lo : res.rev_y;
         }
       }
+    }
+    if constexpr (MODE == 1) {
+      if (!__shfl_sync(0xffffffffu, (int)alive, 31)) break;   // no optimal path below
     }
   }
   // warp reduction

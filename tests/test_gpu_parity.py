@@ -317,3 +317,48 @@ def test_pipelined_host_upload_matches_resident_arena():
     ref = oracle.align_batch_c(arena, table[pick], 11, 1, matrix("blosum62"), threads=16)
     got = np.stack([host[f][pick] for f in FIELDS], axis=1)
     assert (got == ref[:, :7]).all()
+
+
+def test_reverse_box_path_for_every_pair_exact():
+    """PASTIS_SW_TRACEBACK=box sends every pair through the anchored reverse
+    pass (with its dead-strip early stop) + box traceback: still exact on the
+    golden vectors (11 gap settings / matrices) and on skewed config-3 pairs."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+from conftest import FIELDS, expect_tuple, load_golden, matrix
+from paper_2303_01845_b200 import _native, workloads
+from paper_2303_01845_b200.batch import pack_codes, pack_pairs
+from oracle import oracle
+bad = 0
+cases = load_golden("random_pairs.json") + load_golden("kats.json") + load_golden("long_pairs.json")
+groups = {}
+for c in cases:
+    groups.setdefault((c["gap_open"], c["gap_extend"], c["matrix"]), []).append(c)
+for (go, ge, mname), cs in groups.items():
+    batch = pack_pairs([(c["a"], c["b"]) for c in cs])
+    rec, _ = _native.align_host(batch.arena, batch.pairs, _native.make_params(go, ge, matrix(mname)))
+    for c, r in zip(cs, rec):
+        if tuple(int(r[f]) for f in FIELDS) != expect_tuple(c):
+            bad += 1
+sa, sb = workloads.config3(3000, seed=21)
+arena, table = pack_codes(sa, sb)
+m = matrix("blosum62")
+rec, tm = _native.align_host(arena, table, _native.make_params(11, 1, m))
+ref = oracle.align_batch_c(arena, table, 11, 1, m, threads=16)
+got = np.stack([rec[f] for f in FIELDS], axis=1)
+bad += int((got != ref[:, :7]).any(axis=1).sum())
+print(json.dumps({"bad": bad, "n": len(cases) + len(table)}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PASTIS_SW_TRACEBACK="box")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["bad"] == 0, res
