@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pairs", type=int, default=None,
                     help="pairs per GPU (default: the BASELINE config's count)")
-    ap.add_argument("--cpu-sample", type=int, default=3000,
+    ap.add_argument("--cpu-sample", type=int, default=8000,
                     help="pairs in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default=WORKLOAD, choices=["config2", "config3", "config5"],
@@ -164,6 +164,33 @@ class ClockSampler:
                 "sm_max_mhz": float(max(r[2] for r in rows)), "reasons": reasons,
                 "samples": len(inside), "source": self.source,
                 "window": "timed region" if inside else "whole run (no sample inside the timed region)"}
+
+
+def traffic_fields(fwd_ms, args) -> dict:
+    """roofline.traffic: DRAM bytes per K1p launch from the committed ncu
+    --set full capture (profiles/r01/k1p_traffic.json), beside the algorithmic
+    bytes, and the HBM fraction they imply at this run's forward time against
+    MEASURED_PEAKS.json's copy bandwidth."""
+    out = {"traffic": None}
+    if args.workload != "config2" or args.pairs != DEFAULT_PAIRS["config2"]:
+        return out      # the capture is of the default configuration
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "k1p_traffic.json")) as fh:
+            t = json.load(fh)
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm = float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return out
+    per_launch_s = float(np.mean(fwd_ms)) / 1e3 if len(fwd_ms) else 0.0
+    out["traffic"] = t["traffic_bytes_per_launch"]
+    out["traffic_unit"] = "bytes per K1p launch (config 2, 100k pairs; ncu dram__bytes_read+write)"
+    out["algorithmic_bytes_per_launch"] = t["algorithmic_bytes_per_launch"]
+    out["traffic_note"] = t["note"]
+    if per_launch_s > 0:
+        out["hbm_gbs_at_traffic"] = t["traffic_bytes_per_launch"] / per_launch_s / 1e9
+        out["hbm_frac"] = out["hbm_gbs_at_traffic"] / hbm
+        out["hbm_peak_gbs"] = hbm
+    return out
 
 
 def run_reference(args, rank: int, world: int) -> None:
@@ -395,7 +422,7 @@ def main():
                                    "cell (4 adds + 5 maxes); pipe rates measured in tools/microbench",
                      "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 32/(m*n) = 0.0070 B "
                                  "-> non-binding (HBM would allow ~9e14 CUPS)",
-                     "traffic": None},
+                     **traffic_fields(fwd_ms, args)},
         "e2e": {"value": e2e_value, "unit": "GCUPS",
                 "h2d_bytes_per_step": int(arena_np.size + table_np.nbytes),
                 "d2h_bytes_per_step": int(n_pairs * 32),
