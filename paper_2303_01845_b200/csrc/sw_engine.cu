@@ -31,6 +31,7 @@
 #include "sw_kernels.cuh"
 #include "sw_packed.cuh"
 #include "sw_cta.cuh"
+#include "sw_cta_packed.cuh"
 #include "sw_fasta.h"
 #include "sw_kmer.cuh"
 
@@ -97,7 +98,8 @@ struct DeviceCtx {
   cudaEvent_t ev_fork, ev_k1[kNumClasses], ev_tb[kNumClasses];
   KernelInfo fwd[kNumClasses], rev[kNumClasses], box[kNumClasses], ckpt[kNumClasses];
   KernelInfo tb[kNumClasses];
-  KernelInfo fwd_wide, rev_wide, fwd_cta, rev_cta;
+  KernelInfo fwd_wide, rev_wide, fwd_cta, rev_cta, fwd_ctap, jend;
+  DevBuf cta_rows;
   int max_warps = 0;
   size_t pool_want = 0;   // checkpoint bytes the last call asked for (pool growth)
   // host path: the arena is uploaded in slices on copy_stream while the packed
@@ -221,6 +223,20 @@ int get_ctx(int device, DeviceCtx **out) {
     if (rc) return rc;
     rc = setup_cta(k_score_cta<kCtaRowsR, 1>, c->sms, c->rev_cta);
     if (rc) return rc;
+    {
+      const void *fn = (const void *)k_score_cta_packed<kCtaPR>;
+      const int smem = smem_cta_packed(kCtaPR);
+      CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      int nb = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kCtaWarps * 32, smem));
+      if (nb < 1) return fail(SW_ECUDA, "packed CTA kernel cannot be resident");
+      c->fwd_ctap.fn = (KernelFn)k_score_cta_packed<kCtaPR>;
+      c->fwd_ctap.grid = nb * c->sms;
+      c->fwd_ctap.smem = smem;
+      CU(c->cta_rows.ensure((size_t)c->fwd_ctap.grid * kCtaPSlots * kCtaPRowStride * sizeof(uint2)));
+    }
+    rc = setup_kernel(k_jend<kCtaPR>, c->sms, c->jend, c->max_warps);
+    if (rc) return rc;
     // LUT (align.py:27-30) and matrix buffers
     CU(c->lut.ensure(256));
     uint8_t lut[256];
@@ -307,6 +323,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   A.lut = (const uint8_t *)c->lut.p;
   A.ready = ready;
   A.slice_bytes = slice_bytes;
+  A.cta_rows = (uint2 *)c->cta_rows.p;
   A.open_ = prm->gap_open;
   A.ext = prm->gap_extend;
   int smin = 127, smax = -128;
@@ -436,7 +453,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     // long pairs: scalar forward concurrently with the packed classes -- one
     // CTA per pair for pairs of >= 4 strips, one warp per pair for the others
     // (their lists are empty after the first round)
-    c->fwd_cta.fn<<<c->fwd_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 0, kCtaClass);
+    c->fwd_ctap.fn<<<c->fwd_ctap.grid, kCtaWarps * 32, c->fwd_ctap.smem, s>>>(A, 0, kCtaClass);
     c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
         A, 0, kLongClass);
     launches += 2;
@@ -449,7 +466,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
                          cudaMemcpyDeviceToDevice, s));
     c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
         A, 0, kFallbackClass);
-    ++launches;
+    // long pairs the packed CTA kernel had no pool room for, then the j_end
+    // replay of those it did
+    c->fwd_cta.fn<<<c->fwd_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 0, kCtaScalarClass);
+    c->jend.fn<<<c->jend.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 9, 0);
+    launches += 3;
     c->fwd_wide.fn<<<c->fwd_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 3, 0);
     ++launches;
     CU(cudaGetLastError());
@@ -953,7 +974,7 @@ void sw_release(int device) {
     for (DevBuf *b : {&c->arena, &c->codes, &c->pairs, &c->out, &c->st, &c->lists, &c->ctrs,
                       &c->stats, &c->bnd, &c->pool, &c->skeys, &c->svals, &c->cubtmp,
                       &c->km_arena, &c->km_off, &c->km_len, &c->km_base, &c->km_keys, &c->km_runs,
-                      &c->km_pairs, &c->km_out, &c->km_small})
+                      &c->km_pairs, &c->km_out, &c->km_small, &c->cta_rows})
       b->release();
     c->pool_want = 0;
   }

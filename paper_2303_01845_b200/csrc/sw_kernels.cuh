@@ -50,14 +50,18 @@ constexpr int kCtaClass = 0;    // long pairs with >= 4 strips: one CTA per pair
 // concurrently with the packed pass, and a warp that finds a list empty still
 // advances its cursor, so items appended behind it would never be fetched.
 constexpr int kFallbackClass = 1;
+// stage-0 list of long pairs the packed CTA kernel could not take (no pool
+// room for its boundary slots): the scalar one-CTA-per-pair kernel
+constexpr int kCtaScalarClass = 2;
 constexpr int kCtaRowsR = 16;   // rows per lane of the CTA kernels
 constexpr int kCtaStripsMin = 4;
 __host__ __device__ inline int long_class(int m) {
   return (m + 32 * kCtaRowsR - 1) / (32 * kCtaRowsR) >= kCtaStripsMin ? kCtaClass : kLongClass;
 }
-constexpr int kStages = 9;  // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
+constexpr int kStages = 10; // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
                             // 6 K1 with checkpoints, 7 tile traceback,
-                            // 8 K1 with checkpoints deferred to the next round (pool full)
+                            // 8 K1 with checkpoints deferred to the next round (pool full),
+                            // 9 j_end replay of the packed long-pair forward (k_jend)
 constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take the fused path
 constexpr int32_t kScaledLimit = 32767 - 128;
 constexpr int32_t kNegInf = -(1 << 30);
@@ -103,6 +107,7 @@ struct KArgs {
   // have landed (written by the copy stream); nullptr = arena fully resident
   const volatile uint32_t *ready;
   uint64_t slice_bytes;
+  uint2 *cta_rows;         // K1cp: per-CTA ring of strip bottom rows (sw_cta_packed.cuh)
   int2 *bnd;               // per-warp strip boundary rows
   uint64_t bnd_stride;     // int2 per warp
   uint8_t *pool;           // traceback code pool
@@ -343,7 +348,8 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
                                                const int32_t open_, const int32_t ext,
                                                const int32_t best_known, int2 *bnd,
                                                const int lane, uint32_t *ck = nullptr,
-                                               uint32_t *ck_stage = nullptr) {
+                                               uint32_t *ck_stage = nullptr,
+                                               const bool top_from_bnd = false) {
   constexpr int SH = WIDE ? 0 : 16;
   const int32_t OPEN = open_ << SH;
   const int32_t nEXT = -(ext << SH);
@@ -381,7 +387,9 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
     L.botHo = MODE == 1 ? ANC : -OPEN;
     L.botF = MODE == 1 ? ANC : kNegInf;
     L.code_next = lane == 0 ? cols.at(0) : kPad;
-    const bool has_above = strip > 0, has_below = strip + 1 < nstrips;
+    // top_from_bnd: the first strip's row above is given in bnd (a replay of
+    // rows below a saved boundary row, k_jend)
+    const bool has_above = strip > 0 || top_from_bnd, has_below = strip + 1 < nstrips;
     BoundaryReader br;
     const int2 dflt = MODE == 1 ? make_int2(ANC, ANC) : make_int2(-OPEN, kNegInf);
     bool alive = false;   // MODE 1: does the strip's bottom row still carry a live path?

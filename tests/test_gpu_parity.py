@@ -143,15 +143,19 @@ def test_long_multistrip_vs_oracle():
 
 
 def test_wide_path_vs_oracle():
+    """Scores 33k (above the scaled int32 path's 32,640, inside the packed u16
+    paths' headroom) and 66k (above the packed limit: both pairs of the duo
+    re-run in the wide int32 path)."""
     rng = np.random.default_rng(9)
     sa, sb = [], []
-    for n in (2990, 3000, 3100, 3500):
+    for n in (2990, 3000, 6100, 6500):
         a = np.frombuffer(b"W" * n, dtype=np.uint8).copy()
         a[rng.integers(0, n, 20)] = ord("C")
         sa.append(a.tobytes())
         sb.append(a[: n - 7].tobytes())
     rec, tm = _oracle_compare(sa, sb, 11, 1)
-    assert tm["wide_pairs"] >= 3
+    assert tm["wide_pairs"] >= 2
+    assert rec["score"].max() > 65535
 
 
 def test_order_and_sharding_invariance():
@@ -362,3 +366,66 @@ print(json.dumps({"bad": bad, "n": len(cases) + len(table)}))
     assert out.returncode == 0, out.stderr[-2000:]
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["bad"] == 0, res
+
+
+def _long_mix(seed: int, count: int):
+    """Long pairs for the packed CTA path (>= 4 strips of 512 rows): random
+    and homolog pairs of unequal shapes, so a duo mixes lengths and the best
+    cell falls in early or deep strips."""
+    rng = np.random.default_rng(seed)
+    std = np.frombuffer(b"ARNDCQEGHILKMFPSTWYV", np.uint8)
+    sa, sb = [], []
+    for k in range(count):
+        m = int(rng.integers(1600, 4200))
+        a = std[rng.integers(0, 20, m)]
+        if k % 3 == 0:
+            b = std[rng.integers(0, 20, int(rng.integers(1600, 4200)))]
+        else:
+            b = a.copy()
+            mut = rng.random(m) < 0.25
+            b[mut] = std[rng.integers(0, 20, int(mut.sum()))]
+            cut = int(rng.integers(0, m // 2))
+            b = b[cut:cut + int(rng.integers(m // 3, m))]
+        sa.append(a.tobytes())
+        sb.append(b.tobytes())
+    return sa, sb
+
+
+def test_packed_cta_long_pairs_vs_oracle():
+    sa, sb = _long_mix(31, 9)                       # odd: one CTA carries a single pair
+    _oracle_compare(sa, sb, 11, 1)
+    _oracle_compare(sa, sb, 10, 2)
+
+
+def test_packed_cta_no_pool_room_falls_back_exactly():
+    """A 1 MiB pool cannot hold the boundary slots: the duos go to the scalar
+    one-CTA-per-pair kernel, still exact."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+from paper_2303_01845_b200 import _native, blosum62
+from paper_2303_01845_b200.batch import pack_codes
+from oracle import oracle
+rng = np.random.default_rng(32)
+std = np.frombuffer(b"ARNDCQEGHILKMFPSTWYV", np.uint8)
+sa = [std[rng.integers(0, 20, int(rng.integers(1600, 2200)))].tobytes() for _ in range(5)]
+sb = [std[rng.integers(0, 20, int(rng.integers(8000, 9000)))].tobytes() for _ in range(5)]
+arena, table = pack_codes(sa, sb)   # boundary slots: 32 B x 8k+ columns per pair > the pool
+m = np.asarray(blosum62.MATRIX, np.int32)
+rec, tm = _native.align_host(arena, table, _native.make_params(11, 1, m))
+ref = oracle.align_batch_c(arena, table, 11, 1, m, threads=16)
+F = ("score", "i_begin", "i_end", "j_begin", "j_end", "matches", "aln_len")
+got = np.stack([rec[f] for f in F], axis=1)
+print(json.dumps({"bad": int((got != ref[:, :7]).any(axis=1).sum())}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PASTIS_SW_POOL_MB="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert json.loads(out.stdout.strip().splitlines()[-1])["bad"] == 0
