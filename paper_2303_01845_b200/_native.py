@@ -118,7 +118,7 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = path or LIB_PATH
+        p = path or os.environ.get("PASTIS_SW_LIB") or LIB_PATH
         if not os.path.exists(p):
             raise NativeError(
                 f"{p} not found: build the CUDA extension first "

@@ -58,8 +58,8 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
   load_matrix(smat, A.mat);
   uint2 *rows_ring = A.cta_rows + (uint64_t)blockIdx.x * kCtaPSlots * kCtaPRowStride;
   const uint32_t Bs = (uint32_t)A.bias16;
-  const uint32_t BB = A.p_bb, OPEN2 = A.p_open2, EXT2 = A.p_ext2;
-  const uint32_t NEG2 = A.p_ext2, HO0 = A.p_ho0, K2 = A.p_k2;
+  const uint32_t BB = A.p_bb, OPEN2 = A.p_open2;
+  const uint32_t NEG2 = A.p_ext2, HO0 = A.p_ho0, NEXT2 = A.p_next2, NOPEN2 = A.p_nopen2;
   const int lo = A.prof_lo;
   for (;;) {
     if (threadIdx.x == 0) {
@@ -171,22 +171,21 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
           if (lane == 0) { upHo = tHo; upF = tF; }
           uint32_t diag = L.hoUpPrev;
           L.hoUpPrev = upHo;
-          uint32_t F = upF, hoUp = upHo;
+          uint32_t G = upF + OPEN2, tprev = upHo + OPEN2;   // G = F + open (sw_packed.cuh)
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const uint32_t u2 = prmt(word_of(pa, r), word_of(pb, r), sel_pair(r & 3));
-            L.E[r] = vmax2u(L.E[r] - EXT2, L.Ho[r]);
-            const uint32_t D = diag + u2 + K2;
-            const uint32_t t = vmax2u(vmax2u(D, L.E[r]), BB);
-            F = vmax2u(F - EXT2, hoUp);
-            const uint32_t h = vmax2u(t, F);
+            L.E[r] = __viaddmax_u16x2(L.E[r], NEXT2, L.Ho[r]);
+            const uint32_t t = vmax2u(vmax2u(diag + u2, L.E[r]), BB);
+            G = __viaddmax_u16x2(G, NEXT2, tprev);
+            const uint32_t h = __viaddmax_u16x2(G, NOPEN2, t);
             diag = L.Ho[r];
             L.Ho[r] = h - OPEN2;
-            hoUp = t - OPEN2;
+            tprev = t;
             L.rm[r] = vmax2u(L.rm[r], h);
           }
           L.botHo = L.Ho[R - 1];
-          L.botF = F;
+          L.botF = G - OPEN2;
           if (has_below && lane == 31) {
             const int cb = s - 31;
             if (cb >= 0 && cb < n) out_row[cb] = make_uint2(L.botHo, L.botF);

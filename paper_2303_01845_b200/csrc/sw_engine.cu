@@ -331,15 +331,20 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     smin = std::min(smin, (int)prm->matrix[i]);
     smax = std::max(smax, (int)prm->matrix[i]);
   }
-  A.prof_lo = std::min(smin - 1, -1);           // virtual cells score prof_lo < 0
+  // packed passes: u8 profile u = s + open, so D = Ho_diag + u needs no
+  // constant; PAD -> u = 0 (scores -open, never reaches a real cell)
+  A.prof_lo = -prm->gap_open;
   A.bias16 = prm->gap_open + prm->gap_extend + 128;
   A.p_bb = (uint32_t)A.bias16 * 0x10001u;
   A.p_open2 = (uint32_t)prm->gap_open * 0x10001u;
   A.p_ext2 = (uint32_t)prm->gap_extend * 0x10001u;
   A.p_ho0 = A.p_bb - A.p_open2;
-  A.p_k2 = (uint32_t)((prm->gap_open + A.prof_lo) * 0x10001);
-  // packed forward pass needs u8 profile bytes < 128
-  const bool packed_ok = smax - A.prof_lo <= 127;
+  A.p_next2 = (uint32_t)((65536 - prm->gap_extend) & 0xFFFF) * 0x10001u;
+  A.p_nopen2 = (uint32_t)((65536 - prm->gap_open) & 0xFFFF) * 0x10001u;
+  // the packed passes need every u in [0, 127]; other parameter sets
+  // (matrix minimum below -open, or maximum above 127 - open) take the
+  // scalar int32 paths
+  const bool packed_ok = smin >= -prm->gap_open && smax + prm->gap_open <= 127;
 
   CU(cudaEventRecord(c->ev[0], s));
   if (!arena_done) {   // resident arena: encode first, every kernel reads codes
@@ -368,7 +373,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
       return (e && strcmp(e, "cells") == 0) ? 1 : 0;
     }();
     k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
-        A, (unsigned long long *)c->stats.p, env_ckpt && packed_ok, k_in, v_in, sort_cells);
+        A, (unsigned long long *)c->stats.p, env_ckpt && packed_ok, packed_ok, k_in, v_in, sort_cells);
     ++launches;
     CU(cudaGetLastError());
     size_t tmp_bytes = 0;

@@ -55,8 +55,9 @@ constexpr int kFallbackClass = 1;
 constexpr int kCtaScalarClass = 2;
 constexpr int kCtaRowsR = 16;   // rows per lane of the CTA kernels
 constexpr int kCtaStripsMin = 4;
-__host__ __device__ inline int long_class(int m) {
-  return (m + 32 * kCtaRowsR - 1) / (32 * kCtaRowsR) >= kCtaStripsMin ? kCtaClass : kLongClass;
+__host__ __device__ inline int long_class(int m, bool packed_ok = true) {
+  return packed_ok && (m + 32 * kCtaRowsR - 1) / (32 * kCtaRowsR) >= kCtaStripsMin ? kCtaClass
+                                                                                    : kLongClass;
 }
 constexpr int kStages = 10; // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
                             // 6 K1 with checkpoints, 7 tile traceback,
@@ -115,11 +116,11 @@ struct KArgs {
   unsigned long long *pool_top;
   int32_t open_, ext;
   int32_t bias16;           // B: checkpoint values are stored as u16 (v + B)
-  int32_t prof_lo;          // packed profile stores s - prof_lo (0..127); PAD -> 0
+  int32_t prof_lo;          // packed profile stores s - prof_lo = s + open (0..127); PAD -> 0
   // packed (u16x2) constants, precomputed on the host so they live in the
   // constant bank: B, open, ext splatted to both halves, H-open at H=0, and
-  // the D offset (open + prof_lo) * 0x10001
-  uint32_t p_bb, p_open2, p_ext2, p_ho0, p_k2;
+  // -ext, -open per half (for the wrapping per-half adds of VIADDMNMX.U16x2)
+  uint32_t p_bb, p_open2, p_ext2, p_ho0, p_next2, p_nopen2;
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -1283,7 +1284,7 @@ __global__ void k_encode(const uint8_t *__restrict__ raw, uint8_t *__restrict__ 
 // for the packed kernel, which aligns two consecutive pairs per warp) and
 // k_scatter_lists writes the sorted lists.
 constexpr int kNoList = 127;
-__global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt,
+__global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, int packed_ok,
                            unsigned long long *keys, uint32_t *vals, int sort_cells) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned lane = threadIdx.x & 31;
@@ -1303,7 +1304,7 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt,
   const bool fused = allow_ckpt && cells <= kFusedMaxCells;
   // short/medium pairs: packed pass, per length class; long pairs: one
   // scalar class (R = 16), so each long-pair phase has a single tail
-  const int slot = real ? (fused ? 6 * kNumClasses + class_of((int)p.a_len) : long_class((int)p.a_len)) : -1;
+  const int slot = real ? (fused ? 6 * kNumClasses + class_of((int)p.a_len) : long_class((int)p.a_len, packed_ok)) : -1;
   const unsigned peers = __match_any_sync(0xffffffffu, slot);
   const int leader = __ffs(peers) - 1;
   if (slot >= 0 && (int)lane == leader) atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));

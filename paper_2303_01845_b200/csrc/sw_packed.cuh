@@ -3,20 +3,19 @@
 // Same recurrence and wavefront as k_score<FWD> (align.py:103-121), but each
 // 32-bit register holds the same cell of TWO pairs (pair A in the low half,
 // pair B in the high half) as biased unsigned 16-bit values v + B, with
-// B = open + ext + 128.  Measured on B200 (profiles/r01/mix2.txt): plain
-// VIMNMX (s32 or u16x2) issues at full rate on the ALU pipe and co-issues with
-// IMAD (FMA pipe), while the fused DPX ops issue at half rate.  So every add
-// is an IMAD/IADD3 on whole words (the bias keeps both halves in [0, 65535],
-// no borrow crosses a half) and every max is a VIMNMX.U16x2:
-//   E  = max(E - ext, Ho_left)          IMAD + VIMNMX
-//   F  = max(F - ext, Ho_up)            IMAD + VIMNMX
-//   D  = Ho_diag + u + (open + lo)      IADD3  (u = s - lo, 0..127, u8 profile)
-//   h  = max(D, E, F, B)                3 VIMNMX   (B = biased zero: local floor)
+// B = open + ext + 128 (the bias keeps both halves in [0, 65535], so full-word
+// IMAD adds never borrow across halves).  Per row r of a lane (G = F + open):
+//   E  = max(E - ext, Ho_left)          VIADDMNMX.U16x2 (per-half add wraps)
+//   t  = max(Ho_diag + (s + open), E, B)  IMAD + VIMNMX3  (B = biased zero)
+//   G  = max(G - ext, t[r-1])           VIADDMNMX.U16x2 (short F chain: t, not H)
+//   h  = max(G - open, t)               VIADDMNMX.U16x2
 //   Ho = h - open                       IMAD
-//   rowmax = max(rowmax, h)             VIMNMX
-// = ~9 ALU-pipe cycles per 2 cells vs ~10 per cell for the scaled-int32 K1.
-// The score pair comes from the two pairs' int8 profiles with one PRMT (the
-// sign-replicate selector of a byte with msb 0 yields the zero high byte).
+//   rowmax = max(rowmax, h)             VIMNMX.U16x2
+// plus one PRMT merging the two pairs' profile bytes = 8 issue slots per two
+// cells.  A/B on the box (config 2, forward GCUPS): unfused IMAD+VIMNMX for E
+// and F 2,597; fused E+F 2,848; + s+open profile (no IADD3) 2,982; + G form
+// 3,044.  The profile stores u = s + open (0..127: BLOSUM-like matrices with
+// min >= -open; other parameters take the scalar path), so D needs no constant.
 // Per-row maxima give best and i_end (first row reaching best); j_end is found
 // by the traceback kernel from per-window row maxima stored in the column
 // checkpoints (k_tb).  Values are exact while every biased value stays below
@@ -175,10 +174,9 @@ k_score_packed(KArgs A, int stage, int cls) {
   const uint32_t Bs = (uint32_t)A.bias16;
   const uint32_t BB = A.p_bb;
   const uint32_t OPEN2 = A.p_open2;
-  const uint32_t EXT2 = A.p_ext2;
   const uint32_t NEG2 = A.p_ext2;                      // biased "-inf": E/F - ext == 0
   const uint32_t HO0 = A.p_ho0;                        // biased H - open for H == 0
-  const uint32_t K2 = A.p_k2;                          // D = Ho_diag + u + K2
+  const uint32_t NEXT2 = A.p_next2, NOPEN2 = A.p_nopen2;  // per-half -ext, -open
   const int lo = A.prof_lo;
   for (;;) {
     // two consecutive work items per warp
@@ -323,28 +321,25 @@ k_score_packed(KArgs A, int stage, int cls) {
           }
           uint32_t diag = L.hoUpPrev;
           L.hoUpPrev = upHo;
-          uint32_t F = upF, hoUp = upHo;
+          // F carried as G = F + open (biased): G[r] = max(G[r-1] - ext, t[r-1]),
+          // t[-1] = H of the row above; H[r] = max(G[r] - open, t[r]).
+          uint32_t G = upF + OPEN2, tprev = upHo + OPEN2;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            // Short F chain: since open >= ext,
-            //   F[r+1] = max(F[r] - ext, H[r] - open) = max(F[r] - ext, t[r] - open)
-            // with t = max(D, E, 0) off the chain (H[r] = max(t, F[r])).
             const uint32_t u2 = prmt(word_of(pa, r), word_of(pb, r), sel_pair(r & 3));
-            L.E[r] = vmax2u(L.E[r] - EXT2, L.Ho[r]);
-            const uint32_t D = diag + u2 + K2;
-            const uint32_t t = vmax2u(vmax2u(D, L.E[r]), BB);
-            F = vmax2u(F - EXT2, hoUp);
-            const uint32_t h = vmax2u(t, F);
+            L.E[r] = __viaddmax_u16x2(L.E[r], NEXT2, L.Ho[r]);
+            const uint32_t t = vmax2u(vmax2u(diag + u2, L.E[r]), BB);
+            G = __viaddmax_u16x2(G, NEXT2, tprev);
+            const uint32_t h = __viaddmax_u16x2(G, NOPEN2, t);
             diag = L.Ho[r];
             L.Ho[r] = h - OPEN2;
-            hoUp = t - OPEN2;
+            tprev = t;
             L.rm[r] = vmax2u(L.rm[r], h);
           }
           L.botHo = L.Ho[R - 1];
-          L.botF = F;
-          hoUp = L.botHo;
-          stageA[bslot + q] = prmt(hoUp, F, 0x5410u);
-          stageB[bslot + q] = prmt(hoUp, F, 0x7632u);
+          L.botF = G - OPEN2;
+          stageA[bslot + q] = prmt(L.botHo, L.botF, 0x5410u);
+          stageB[bslot + q] = prmt(L.botHo, L.botF, 0x7632u);
         }
         __syncwarp();
         if (flA) flA[s0 / 4] = reinterpret_cast<const uint4 *>(stageA)[lane];
