@@ -118,6 +118,8 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
         ringA[c & 127] = (c >= 0 && c < n0) ? (uint8_t)cols0.at(c) : (uint8_t)kPad;
         ringB[c & 127] = (c >= 0 && c < n1) ? (uint8_t)cols1.at(c) : (uint8_t)kPad;
       }
+      int nxtA = 96 + lane < n0 ? cols0.at(96 + lane) : kPad;   // next refill, loaded ahead
+      int nxtB = 96 + lane < n1 ? cols1.at(96 + lane) : kPad;
       __syncwarp();
       PackedLane<R> L;
 #pragma unroll
@@ -141,8 +143,10 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
         if ((s0 & 31) == 0) {
           if (s0 > 0) {    // refill column-code ring slots for columns s0+64 .. s0+95
             const int c = s0 + 64 + lane;
-            ringA[c & 127] = (c < n0) ? (uint8_t)cols0.at(c) : (uint8_t)kPad;
-            ringB[c & 127] = (c < n1) ? (uint8_t)cols1.at(c) : (uint8_t)kPad;
+            ringA[c & 127] = (uint8_t)nxtA;
+            ringB[c & 127] = (uint8_t)nxtB;
+            nxtA = c + 32 < n0 ? cols0.at(c + 32) : kPad;
+            nxtB = c + 32 < n1 ? cols1.at(c + 32) : kPad;
           }
           if (has_above && s0 < n) {
             const int need = min(s0 + 32, n);
