@@ -42,7 +42,7 @@ constexpr int kProfBytes = kCodes * kProfStride;  // 13,312 B per warp
 constexpr int kMatBytes = 688;           // 26*26 int8, padded to 16
 constexpr int kStageBytes = 16 * 8 * 4;  // per-warp row-checkpoint staging (16 boundaries x 8 steps)
 constexpr int kWarpsPerBlock = 4;
-constexpr int kNumClasses = 6;
+constexpr int kNumClasses = 7;
 constexpr int kLongClass = kNumClasses - 1;  // R = 16: the only class of the long-pair path
 constexpr int kCtaClass = 0;    // long pairs with >= 4 strips: one CTA per pair (sw_cta.cuh)
 // stage-0 list of the packed pass's no-checkpoint-room fallbacks.  Kept apart
@@ -67,10 +67,11 @@ constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take t
 constexpr int32_t kScaledLimit = 32767 - 128;
 constexpr int32_t kNegInf = -(1 << 30);
 
-// Length classes: R rows per lane, 32R rows per strip.  A pair with m rows
-// takes the class whose strips pad m the least (ties: larger R, fewer strips).
+// Length classes: R rows per lane, 32R rows per strip.  class_of (box
+// traceback lists): the class whose strips pad m the least (ties: larger R,
+// fewer strips).  packed_class_of (packed forward): the least modelled cost.
 __host__ __device__ constexpr int class_rows(int cls) {
-  return cls == 0 ? 4 : cls == 1 ? 6 : cls == 2 ? 8 : cls == 3 ? 10 : cls == 4 ? 12 : 16;
+  return cls == 0 ? 4 : cls == 1 ? 6 : cls == 2 ? 7 : cls == 3 ? 8 : cls == 4 ? 9 : cls == 5 ? 10 : 16;
 }
 __host__ __device__ inline int class_of(int m) {
   int best = kNumClasses - 1;
@@ -79,6 +80,25 @@ __host__ __device__ inline int class_of(int m) {
     const long rows_per_strip = 32L * class_rows(c);
     const long rows = (m + rows_per_strip - 1) / rows_per_strip * rows_per_strip;
     if (rows < best_rows) { best_rows = rows; best = c; }
+  }
+  return best;
+}
+// Issue-slot model of the packed forward (k_score_packed<R>, profiled on the
+// box): per strip, n + 31 wavefront steps of ~9R + 23 instructions (9 per
+// packed row-word + ~23 per step: shuffles, profile/ring loads, row
+// checkpoints), ~6 more per step when the row above comes from the previous
+// strip, and ~260R to build the strip's profile; classes whose profiles
+// limit residency to 2 blocks/SM (R >= 12) pay x1.5.
+__host__ __device__ inline int packed_class_of(int m, int n) {
+  int best = 0;
+  float best_cost = 3.4e38f;
+  for (int c = 0; c < kNumClasses; ++c) {
+    const int R = class_rows(c);
+    const int S = (m + 32 * R - 1) / (32 * R);
+    float cost = (float)S * (float)(n + 31) * (float)(9 * R + 23) +
+                 (float)(S - 1) * (float)(n + 31) * 6.f + (float)S * 260.f * (float)R;
+    if (R >= 12) cost *= 1.5f;
+    if (cost < best_cost) { best_cost = cost; best = c; }
   }
   return best;
 }
@@ -1304,7 +1324,8 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
   const bool fused = allow_ckpt && cells <= kFusedMaxCells;
   // short/medium pairs: packed pass, per length class; long pairs: one
   // scalar class (R = 16), so each long-pair phase has a single tail
-  const int slot = real ? (fused ? 6 * kNumClasses + class_of((int)p.a_len) : long_class((int)p.a_len, packed_ok)) : -1;
+  const int slot = real ? (fused ? 6 * kNumClasses + packed_class_of((int)p.a_len, (int)p.b_len)
+                                   : long_class((int)p.a_len, packed_ok)) : -1;
   const unsigned peers = __match_any_sync(0xffffffffu, slot);
   const int leader = __ffs(peers) - 1;
   if (slot >= 0 && (int)lane == leader) atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));

@@ -32,14 +32,28 @@ constexpr int kRingBytes = 2 * 128;              // column-code rings of the two
 constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
 
 // u8 profile of one pair: part 0 = [code][lane][P0] (P0 = 4 or 8 bytes),
-// part 1 = [code][lane][P1] for the remaining rows (R = 10 -> 8 + 2 bytes).
-__host__ __device__ constexpr int prof_p0(int R) { return R <= 4 ? 4 : 8; }
-__host__ __device__ constexpr int prof_p1(int R) { return R <= 8 ? 0 : (R <= 10 ? 2 : (R <= 12 ? 4 : 8)); }
+// part 1 = [code][lane][P1] for the remaining rows (R = 10 -> 8 + 2 bytes,
+// R = 6 -> 4 + 2).  Rows 4k..4k+3 live in word k of the loaded uint4.
+__host__ __device__ constexpr int prof_p0(int R) { return R <= 6 ? 4 : 8; }
+__host__ __device__ constexpr int prof_p1(int R) {
+  return R <= 4 ? 0 : R <= 6 ? 2 : R <= 8 ? 0 : R <= 10 ? 2 : R <= 12 ? 4 : 8;
+}
 __host__ __device__ constexpr int prof_bytes_p(int R) { return kCodes * 32 * (prof_p0(R) + prof_p1(R)); }
 __host__ __device__ constexpr int warp_bytes_p(int R) {
   return (2 * prof_bytes_p(R) + kStageBytesP + kRingBytes + 15) / 16 * 16;
 }
 __host__ __device__ constexpr int smem_packed(int R) { return kMatBytes + kWarpsPerBlockP * warp_bytes_p(R); }
+// resident blocks per SM the packed forward is compiled for (registers):
+// small R has little per-lane state, so more warps hide the latency
+#ifndef K1P_MINB_SMALL
+#define K1P_MINB_SMALL 6
+#endif
+#ifndef K1P_MINB_MID
+#define K1P_MINB_MID 4
+#endif
+__host__ __device__ constexpr int packed_min_blocks(int R) {
+  return R <= 4 ? K1P_MINB_SMALL : R <= 6 ? K1P_MINB_MID : 3;
+}
 
 __device__ __forceinline__ uint32_t vmax2u(uint32_t a, uint32_t b) {
   uint32_t d;
@@ -72,10 +86,11 @@ __device__ __forceinline__ void build_profile_u8(uint8_t *prof, const int8_t *ma
     if (P0 == 4) *reinterpret_cast<uint32_t *>(p0) = w[0];
     else *reinterpret_cast<uint2 *>(p0) = make_uint2(w[0], w[1]);
     if (P1 > 0) {
+      constexpr int k1 = P0 / 4;       // first word of part 1
       uint8_t *p1 = prof + kCodes * 32 * P0 + (code * 32 + lane) * P1;
-      if (P1 == 2) *reinterpret_cast<uint16_t *>(p1) = (uint16_t)w[2];
-      else if (P1 == 4) *reinterpret_cast<uint32_t *>(p1) = w[2];
-      else *reinterpret_cast<uint2 *>(p1) = make_uint2(w[2], w[3]);
+      if (P1 == 2) *reinterpret_cast<uint16_t *>(p1) = (uint16_t)w[k1];
+      else if (P1 == 4) *reinterpret_cast<uint32_t *>(p1) = w[k1];
+      else *reinterpret_cast<uint2 *>(p1) = make_uint2(w[k1], w[k1 + 1]);
     }
   }
 }
@@ -95,13 +110,16 @@ __device__ __forceinline__ uint4 load_profile_u8(const uint8_t *prof, int code, 
   }
   if (P1 > 0) {
     const uint8_t *p1 = prof + kCodes * 32 * P0 + (code * 32 + lane) * P1;
-    if (P1 == 2) v.z = *reinterpret_cast<const uint16_t *>(p1);
-    else if (P1 == 4) v.z = *reinterpret_cast<const uint32_t *>(p1);
+    uint32_t a = 0u, b = 0u;
+    if (P1 == 2) a = *reinterpret_cast<const uint16_t *>(p1);
+    else if (P1 == 4) a = *reinterpret_cast<const uint32_t *>(p1);
     else {
-      const uint2 b = *reinterpret_cast<const uint2 *>(p1);
-      v.z = b.x;
-      v.w = b.y;
+      const uint2 q = *reinterpret_cast<const uint2 *>(p1);
+      a = q.x;
+      b = q.y;
     }
+    if (P0 == 4) v.y = a;            // part 1 continues at word P0 / 4
+    else { v.z = a; v.w = b; }
   }
   return v;
 }
@@ -159,7 +177,7 @@ struct PackedPair {        // one of the two pairs a warp carries
 };
 
 template <int R>
-__global__ void __launch_bounds__(kWarpsPerBlockP * 32, 3)
+__global__ void __launch_bounds__(kWarpsPerBlockP * 32, packed_min_blocks(R))
 k_score_packed(KArgs A, int stage, int cls) {
   extern __shared__ __align__(16) uint8_t smem[];
   int8_t *smat = reinterpret_cast<int8_t *>(smem);
