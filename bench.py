@@ -49,8 +49,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pairs", type=int, default=None,
                     help="pairs per GPU (default: the BASELINE config's count)")
-    ap.add_argument("--cpu-sample", type=int, default=8000,
-                    help="pairs in the bounded CPU-baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=64000,
+                    help="pairs in the bounded CPU-baseline sample (~12 s on 16 cores)")
+    ap.add_argument("--ref-sample", type=int, default=4000,
+                    help="pairs per step of --impl reference (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default=WORKLOAD, choices=["config2", "config3", "config5"],
                     help="exploration only; the headline bench is config2")
@@ -201,7 +203,7 @@ def run_reference(args, rank: int, world: int) -> None:
     vals = []
     last = None
     for step in range(args.warmup + args.steps):
-        r = cpu_bench("numpy", max(200, args.cpu_sample // 2), seed=2303 + step)
+        r = cpu_bench("numpy", args.ref_sample, seed=2303 + step)
         if step >= args.warmup:
             vals.append(r["gcups"])
             last = r
