@@ -133,6 +133,25 @@ def test_random_lengths_and_gaps_vs_oracle():
         _oracle_compare(sa, sb, go, ge)
 
 
+def test_packed_class_boundaries_vs_oracle():
+    """Row counts at and around every packed class's strip multiples (32R rows,
+    R = 4, 6, 7, 8, 9, 10, 16; the cost model picks the class per (m, n)),
+    each with homologous and unrelated columns of several widths."""
+    rng = np.random.default_rng(77)
+    ms = sorted({v + d for R in (4, 6, 7, 8, 9, 10, 16) for k in (1, 2, 3)
+                 for v in (32 * R * k,) for d in (-1, 0, 1) if 0 < v + d <= 2100})
+    sa, sb = [], []
+    for m in ms:
+        a = workloads._random_seq(rng, m)
+        for n in (1, 33, 300, m):
+            b = (workloads._fit(rng, workloads._homolog(rng, a, 0.15, 0.04), n)
+                 if rng.random() < 0.6 else workloads._random_seq(rng, n))
+            sa.append(a.tobytes())
+            sb.append(b.tobytes())
+    for ge in (1, 2):
+        _oracle_compare(sa, sb, 11, ge)
+
+
 def test_long_multistrip_vs_oracle():
     sa, sb = workloads.config5(6, seed=3, lo=2000, hi=5000)
     rng = np.random.default_rng(4)
