@@ -53,6 +53,7 @@ extern "C" {
 #define SW_STATUS_OK 0
 #define SW_STATUS_EMPTY 1     /* empty sequence: AlignmentError (align.py:81-82) */
 #define SW_STATUS_INTERNAL 2  /* traceback lost: AssertionError (align.py:150) */
+#define SW_STATUS_INVALID 3   /* pair outside the arena / > 65000 residues: the call returns SW_EINVAL */
 
 typedef struct sw_pair_t { /* one candidate pair; a = rows, b = columns */
   uint64_t a_off;          /* byte offset of sequence a in the arena */

@@ -320,6 +320,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   A.lists = (uint32_t *)c->lists.p;
   A.ctrs = (uint32_t *)c->ctrs.p;
   A.n_pairs = n_pairs;
+  A.arena_bytes = arena_bytes;
   A.lut = (const uint8_t *)c->lut.p;
   A.ready = ready;
   A.slice_bytes = slice_bytes;
@@ -545,10 +546,13 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     if (pround >= 1024) return fail(SW_EINTERNAL, "checkpoint pool too small for the batch");
   }
   CU(cudaEventRecord(c->ev[12], s));
-  unsigned long long hstats[5] = {0ull, 0ull, 0ull, 0ull, 0ull};
+  unsigned long long hstats[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
   CU(cudaMemcpyAsync(hstats, c->stats.p, sizeof(hstats), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   if (hstats[4] > c->pool.bytes) c->pool_want = (size_t)hstats[4];   // grow on the next call
+  if (hstats[5])
+    return fail(SW_EINVAL, std::to_string(hstats[5]) +
+                               " pair(s) reference bytes outside the arena or exceed 65000 residues");
   if (tm) {
     tm->forward_ms += fwd_ms;
     tm->reverse_ms += rev_ms;
@@ -569,18 +573,14 @@ int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_
   int rc = check_params(params);
   if (rc) return rc;
   if (n_pairs && (!pairs || !out)) return fail(SW_EINVAL, "NULL pairs/out");
-  for (uint64_t k = 0; k < n_pairs; ++k) {
-    const sw_pair_t &p = pairs[k];
-    if (p.a_off + p.a_len > arena_bytes || p.b_off + p.b_len > arena_bytes)
-      return fail(SW_EINVAL, "pair references bytes outside the arena");
-    if (p.a_len > 65000 || p.b_len > 65000)
-      return fail(SW_EINVAL, "sequence longer than 65000 residues");
-  }
+  // pair bounds are checked on the device by k_classify (no host pass over the table)
+  const double t_valid = now_ms();
   DeviceCtx *c = nullptr;
   rc = get_ctx(device, &c);
   if (rc) return rc;
   std::lock_guard<std::mutex> g(c->mu);
   CU(cudaSetDevice(device));
+  const double t_ctx = now_ms();
   if (tm) memset(tm, 0, sizeof(*tm));
   if (n_pairs == 0) return SW_OK;
   cudaStream_t s = c->stream;
@@ -595,6 +595,7 @@ int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_
   const uint64_t slice = std::max<uint64_t>((uint64_t)4 << 20,
                                             (arena_bytes + kMaxSlices - 1) / kMaxSlices);
   const int nslices = (int)((arena_bytes + slice - 1) / slice);
+  const double t_ev8 = now_ms();
   CU(cudaEventRecord(c->ev[8], s));
   CU(cudaStreamWaitEvent(cs, c->ev[8], 0));
   CU(cudaMemsetAsync(c->readyb.p, 0, 4, cs));
@@ -614,7 +615,14 @@ int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_
   CU(cudaEventRecord(c->ev[10], s));
   CU(cudaMemcpyAsync(out, c->out.p, n_pairs * sizeof(sw_result_t), cudaMemcpyDeviceToHost, s));
   CU(cudaEventRecord(c->ev[11], s));
+  const double t_issued = now_ms();
   CU(cudaStreamSynchronize(s));
+  if (getenv("PASTIS_SW_DEBUG_E2E")) {
+    fprintf(stderr, "e2e: valid=%.3f ctx=%.3f ev8=%.3f ", t_valid - t0, t_ctx - t0, t_ev8 - t0);
+    fprintf(stderr, "e2e: host_issue=%.3f pre_kernel(ev8->ev0)=%.3f kernel(ev0->ev10)=%.3f d2h=%.3f wall=%.3f\n",
+            t_issued - t0, ev_ms(c->ev[8], c->ev[0]), ev_ms(c->ev[0], c->ev[10]),
+            ev_ms(c->ev[10], c->ev[11]), now_ms() - t0);
+  }
   if (tm) {
     tm->h2d_ms = ev_ms(c->ev[8], c->ev_arena);   // overlaps the forward pass
     tm->d2h_ms = ev_ms(c->ev[10], c->ev[11]);
@@ -922,7 +930,7 @@ int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena
   for (uint64_t k = 0; k < n_pairs; ++k) {
     const sw_pair_t &p = pairs[k];
     if (p.a_off + p.a_len > arena_bytes || p.b_off + p.b_len > arena_bytes)
-      return fail(SW_EINVAL, "pair references bytes outside the arena");
+      return fail(SW_EINVAL, "pair references bytes outside the arena");   // before any read
     Shard &S = sh[shard[k]];
     sw_pair_t q = p;
     q.a_off = place(S, seen[shard[k]], p.a_off, p.a_len);

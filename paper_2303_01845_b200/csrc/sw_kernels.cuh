@@ -104,7 +104,7 @@ __host__ __device__ inline int packed_class_of(int m, int n) {
 }
 __host__ __device__ constexpr int box_lane_bytes(int R) { return R <= 4 ? 2 : R <= 8 ? 4 : 8; }
 
-enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4, kFlagNeedJ = 8 };
+enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4, kFlagNeedJ = 8, kFlagInvalid = 16 };
 
 struct PairState {         // per-pair scratch between the passes (48 B)
   int32_t best, i_end, j_end, flags;
@@ -123,6 +123,7 @@ struct KArgs {
   uint32_t *lists;         // [kStages][kNumClasses][n_pairs]
   uint32_t *ctrs;          // count[kStages*kNumClasses], cursor[...] after it
   uint64_t n_pairs;
+  uint64_t arena_bytes;     // pairs must lie inside [0, arena_bytes) (checked by k_classify)
   const uint8_t *lut;      // raw byte -> residue code (align.py:27-30), 256 entries
   // host-pipelined arenas: ready = number of arena slices of slice_bytes that
   // have landed (written by the copy stream); nullptr = arena fully resident
@@ -1218,6 +1219,11 @@ __global__ void k_walk(KArgs A, const uint32_t *only, uint32_t n_only) {
   sw_result_t r;
   r.score = 0; r.i_begin = r.i_end = r.j_begin = r.j_end = -1;
   r.matches = 0; r.aln_len = 0; r.status = SW_STATUS_OK;
+  if (A.st[k].flags & kFlagInvalid) {
+    r.status = SW_STATUS_INVALID;
+    A.out[k] = r;
+    return;
+  }
   if (p.a_len == 0 || p.b_len == 0) {
     r.status = SW_STATUS_EMPTY;
     A.out[k] = r;
@@ -1317,6 +1323,16 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
     PairState s;
     s.best = 0; s.i_end = s.j_end = -1; s.flags = 0; s.i0 = s.j0 = 0; s.box_cls = 0;
     s.box_n = 0; s.code_off = 0; s.box_m = 0; s.pad = 0;
+    // the call's only bounds check (sw_align_batch and the device entry point):
+    // a pair outside the arena or longer than 65,000 residues is never
+    // scheduled; the call then fails with SW_EINVAL
+    if (p.a_off + p.a_len > A.arena_bytes || p.b_off + p.b_len > A.arena_bytes ||
+        p.a_len > 65000u || p.b_len > 65000u) {
+      s.flags = kFlagInvalid;
+      atomicAdd(&stats[5], 1ull);
+      p.a_len = 0;
+      p.b_len = 0;
+    }
     A.st[k] = s;
   }
   const bool real = in && p.a_len > 0 && p.b_len > 0;

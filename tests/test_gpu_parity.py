@@ -152,6 +152,24 @@ def test_packed_class_boundaries_vs_oracle():
         _oracle_compare(sa, sb, 11, ge)
 
 
+def test_invalid_pairs_fail_the_call_and_the_next_call_is_exact():
+    """Pairs outside the arena (or longer than 65,000 residues) are rejected on
+    the device by the planning kernel: the call raises (SW_EINVAL) without
+    touching them, and the engine stays usable."""
+    sa, sb = workloads.config2(64, seed=5)
+    arena, table = pack_codes(sa, sb)
+    p = _native.make_params(11, 1, matrix("blosum62"))
+    bad = table.copy()
+    bad["b_off"][7] = arena.size          # one byte past the end
+    with pytest.raises(ValueError, match="outside the arena"):
+        _native.align_host(arena, bad, p)
+    long = table.copy()
+    long["a_len"][3] = 65001
+    with pytest.raises(ValueError):
+        _native.align_host(arena, long, p)
+    _oracle_compare(sa, sb, 11, 1)
+
+
 def test_long_multistrip_vs_oracle():
     sa, sb = workloads.config5(6, seed=3, lo=2000, hi=5000)
     rng = np.random.default_rng(4)
