@@ -379,13 +379,13 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(cudaGetLastError());
     size_t tmp_bytes = 0;
     CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out,
-                                       (int)n_pairs, 0, 55, s));
+                                       (int)n_pairs, 0, list_key_shift(sort_cells) + 7, s));
     CU(c->cubtmp.ensure(tmp_bytes));
     CU(cub::DeviceRadixSort::SortPairs(c->cubtmp.p, tmp_bytes, k_in, k_out, v_in, v_out,
-                                       (int)n_pairs, 0, 55, s));
+                                       (int)n_pairs, 0, list_key_shift(sort_cells) + 7, s));
     launches += 4;
     k_scatter_lists<<<(unsigned)std::min<uint64_t>((n_pairs + 255) / 256, (uint64_t)c->sms * 8), 256,
-                      0, s>>>(A, k_out, v_out);
+                      0, s>>>(A, k_out, v_out, list_key_shift(sort_cells));
     ++launches;
     CU(cudaGetLastError());
   }

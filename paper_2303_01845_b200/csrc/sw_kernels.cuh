@@ -1310,6 +1310,9 @@ __global__ void k_encode(const uint8_t *__restrict__ raw, uint8_t *__restrict__ 
 // for the packed kernel, which aligns two consecutive pairs per warp) and
 // k_scatter_lists writes the sorted lists.
 constexpr int kNoList = 127;
+// sort key = list (7 bits) above the order field: the 32-bit shape order by
+// default (a 39-bit key: 5 radix passes), a 48-bit cell count otherwise
+__host__ __device__ constexpr int list_key_shift(int sort_cells) { return sort_cells ? 48 : 32; }
 __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, int packed_ok,
                            unsigned long long *keys, uint32_t *vals, int sort_cells) {
   const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1350,7 +1353,7 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
         sort_cells ? ((0xFFFFFFFFFFFFull - cells) & 0xFFFFFFFFFFFFull)
                    : (((unsigned long long)(0xFFFFu - min(p.a_len, 0xFFFFu)) << 16) |
                       (unsigned long long)(0xFFFFu - min(p.b_len, 0xFFFFu)));
-    keys[k] = ((unsigned long long)(slot >= 0 ? slot : kNoList) << 48) | order;
+    keys[k] = ((unsigned long long)(slot >= 0 ? slot : kNoList) << list_key_shift(sort_cells)) | order;
     vals[k] = (uint32_t)k;
   }
   unsigned long long c = real ? cells : 0ull;
@@ -1369,7 +1372,8 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
 
 // Sorted (key, pair) -> per-list arrays; list offsets are the exclusive
 // prefix of the list counts in key order (lists are contiguous in the sort).
-__global__ void k_scatter_lists(KArgs A, const unsigned long long *keys, const uint32_t *vals) {
+__global__ void k_scatter_lists(KArgs A, const unsigned long long *keys, const uint32_t *vals,
+                                int key_shift) {
   __shared__ uint32_t off[kStages * kNumClasses];
   if (threadIdx.x == 0) {
     uint32_t acc = 0;
@@ -1381,7 +1385,7 @@ __global__ void k_scatter_lists(KArgs A, const unsigned long long *keys, const u
   __syncthreads();
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < A.n_pairs;
        p += (uint64_t)gridDim.x * blockDim.x) {
-    const int slot = (int)(keys[p] >> 48);
+    const int slot = (int)(keys[p] >> key_shift);
     if (slot >= kStages * kNumClasses) continue;
     A.lists[(uint64_t)slot * A.n_pairs + (p - off[slot])] = vals[p];
   }
