@@ -105,6 +105,8 @@ struct DeviceCtx {
   // host path: the arena is uploaded in slices on copy_stream while the packed
   // forward already runs; `ready` counts the slices that have landed
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t pstream = nullptr;          // greatest priority: run_device's chain
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaEvent_t ev_pairs = nullptr, ev_arena = nullptr;
   DevBuf readyb;
   uint32_t *slice_vals = nullptr;   // pinned 1..kMaxSlices
@@ -199,13 +201,23 @@ int get_ctx(int device, DeviceCtx **out) {
     CU(cudaSetDevice(device));
     c->device = device;
     CU(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
-    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // The call's serial chain (planning, the scalar long-pair kernels, the
+    // box traceback, the walk) runs on a greatest-priority stream, the
+    // length classes on least-priority streams: pending blocks of the chain
+    // are scheduled first whenever a class kernel frees an SM, so the chain
+    // is not queued behind the classes' persistent grids.
+    int prio_least = 0, prio_greatest = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+    CU(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_greatest));
+    CU(cudaStreamCreateWithPriority(&c->pstream, cudaStreamNonBlocking, prio_greatest));
+    CU(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
     for (auto &e : c->ev) CU(cudaEventCreate(&e));
     CU(cudaEventCreate(&c->ev_fork));
     for (int k = 0; k < kNumClasses; ++k) {
-      CU(cudaStreamCreateWithFlags(&c->cstream[k], cudaStreamNonBlocking));
+      CU(cudaStreamCreateWithPriority(&c->cstream[k], cudaStreamNonBlocking, prio_least));
       CU(cudaEventCreate(&c->ev_k1[k]));
-      CU(cudaEventCreateWithFlags(&c->ev_tb[k], cudaEventDisableTiming));
+      CU(cudaEventCreate(&c->ev_tb[k]));
     }
     CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&c->ev_pairs, cudaEventDisableTiming));
@@ -290,6 +302,13 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
                cudaEvent_t arena_done = nullptr) {
   if (n_pairs == 0) return SW_OK;
   if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
+  // the chain runs on the greatest-priority stream, joined back to `s` at the end
+  cudaStream_t user_s = s;
+  if (s != c->stream) {
+    s = c->pstream;
+    CU(cudaEventRecord(c->ev_in, user_s));
+    CU(cudaStreamWaitEvent(s, c->ev_in, 0));
+  }
   uint32_t launches = 0;
   const double h0 = now_ms();
   // device buffers
@@ -535,6 +554,13 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     // forward = the forward passes that run concurrently after the fork: the
     // packed classes (their own streams) and the scalar long-pair pass (main
     // stream); the scalar fallback re-run is not included (it is in kernel_ms)
+    if (getenv("PASTIS_SW_DEBUG_E2E")) {   // per-class completion times (debug aid)
+      fprintf(stderr, "round %d: main-fwd %.2f |", pround, ev_ms(c->ev_fork, c->ev[7]));
+      for (int cls = 0; cls < kNumClasses; ++cls)
+        fprintf(stderr, " R%d k1 %.2f tb %.2f (n=%u) |", class_rows(cls), ev_ms(c->ev_fork, c->ev_k1[cls]),
+                ev_ms(c->ev_fork, c->ev_tb[cls]), h_cnt[6 * kNumClasses + cls]);
+      fprintf(stderr, "\n");
+    }
     double f = ev_ms(c->ev_fork, c->ev[7]);
     for (int cls = 0; cls < kNumClasses; ++cls) f = std::max(f, (double)ev_ms(c->ev_fork, c->ev_k1[cls]));
     fwd_ms += f;
@@ -563,6 +589,10 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     tm->wide_pairs += wide;
     tm->host_plan_ms += h1 - h0;
     tm->host_setup_ms += h2 - h1;
+  }
+  if (s != user_s) {
+    CU(cudaEventRecord(c->ev_out, s));
+    CU(cudaStreamWaitEvent(user_s, c->ev_out, 0));
   }
   return SW_OK;
 }
