@@ -73,7 +73,7 @@ struct DevBuf {
   }
 };
 
-constexpr int kSmemScore = kMatBytes + kWarpsPerBlock * (kProfBytes + kStageBytes);
+constexpr int kSmemScore = kMatBytes + kWarpsPerBlock * kProfBytes;
 
 typedef void (*KernelFn)(KArgs, int, int);
 

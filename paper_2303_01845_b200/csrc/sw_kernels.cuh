@@ -40,7 +40,6 @@ constexpr int kLaneBytes = 16;           // profile bytes per lane per code (R <
 constexpr int kProfStride = 32 * kLaneBytes;
 constexpr int kProfBytes = kCodes * kProfStride;  // 13,312 B per warp
 constexpr int kMatBytes = 688;           // 26*26 int8, padded to 16
-constexpr int kStageBytes = 16 * 8 * 4;  // per-warp row-checkpoint staging (16 boundaries x 8 steps)
 constexpr int kWarpsPerBlock = 4;
 constexpr int kNumClasses = 7;
 constexpr int kLongClass = kNumClasses - 1;  // R = 16: the only class of the long-pair path
@@ -104,13 +103,15 @@ __host__ __device__ inline int packed_class_of(int m, int n) {
 }
 __host__ __device__ constexpr int box_lane_bytes(int R) { return R <= 4 ? 2 : R <= 8 ? 4 : 8; }
 
-enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4, kFlagNeedJ = 8, kFlagInvalid = 16 };
+enum : int32_t { kFlagWide = 1, kFlagRetry = 2, kFlagDone = 4, kFlagNeedJ = 8, kFlagInvalid = 16,
+                 kFlagHi = 32 };  // kFlagHi: the pair is the high half of its duo's row checkpoints
 
 struct PairState {         // per-pair scratch between the passes (48 B)
   int32_t best, i_end, j_end, flags;
   int32_t i0, j0, box_cls, box_n;  // traceback-code box origin, class (R) and width
   uint64_t code_off;               // byte offset of the box's codes in the pool
-  int32_t box_m, pad;
+  int32_t box_m;
+  uint32_t row_delta;              // packed path: duo row checkpoints at code_off + row_delta
 };
 
 struct KArgs {
@@ -267,7 +268,8 @@ struct BoundaryReader {
 // ---------------------------------------------------------------------------
 struct CkLayout {
   int G, nb, nwin, spad;
-  uint32_t col_words, strip_words;
+  uint32_t col_words;   // per pair and strip: column checkpoints
+  uint32_t row_words;   // per duo and strip: row checkpoints, [boundary][step][2] words
 };
 __host__ __device__ inline CkLayout ck_layout(int R, int n) {
   CkLayout L;
@@ -276,7 +278,7 @@ __host__ __device__ inline CkLayout ck_layout(int R, int n) {
   L.nwin = (n + 31 + 31) / 32;
   L.spad = L.nwin * 32;
   L.col_words = (uint32_t)L.nwin * 32u * (uint32_t)(2 * R + 1);
-  L.strip_words = L.col_words + (uint32_t)L.nb * (uint32_t)L.spad;
+  L.row_words = 2u * (uint32_t)L.nb * (uint32_t)L.spad;
   return L;
 }
 // boundary index of lane t (-1 when t is not a boundary lane)
@@ -369,9 +371,7 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
                                                const View cols, const int m, const int n,
                                                const int32_t open_, const int32_t ext,
                                                const int32_t best_known, int2 *bnd,
-                                               const int lane, uint32_t *ck = nullptr,
-                                               uint32_t *ck_stage = nullptr,
-                                               const bool top_from_bnd = false) {
+                                               const int lane, const bool top_from_bnd = false) {
   constexpr int SH = WIDE ? 0 : 16;
   const int32_t OPEN = open_ << SH;
   const int32_t nEXT = -(ext << SH);
@@ -417,52 +417,14 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
     bool alive = false;   // MODE 1: does the strip's bottom row still carry a live path?
     if (has_above) br.init(bnd, n, lane, dflt);
     const int steps = n + 31;
-    // checkpoints (forward pass of short/medium pairs): column checkpoints are
-    // written directly (coalesced, once per 32 steps); row checkpoints are
-    // staged 8 steps at a time in shared memory (stage[b][8]) and flushed as
-    // full 32-byte sectors
-    uint32_t *ck_col = nullptr, *stage_slot = nullptr;
-    uint4 *flush_dst = nullptr;
-    int ck_nwin = 0;
-    if (!WIDE && MODE == 0 && ck) {
-      const CkLayout CL = ck_layout(R, n);
-      uint32_t *base = ck + (uint64_t)strip * CL.strip_words;
-      ck_col = base + lane;
-      const int b = ck_boundary(lane, CL);
-      if (b >= 0) stage_slot = ck_stage + b * kScoreUnroll;
-      if (lane < 2 * CL.nb)
-        flush_dst = reinterpret_cast<uint4 *>(base + CL.col_words + (uint32_t)(lane >> 1) * CL.spad) +
-                    (lane & 1);
-      ck_nwin = CL.nwin;
-    }
     for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
 #pragma unroll 2
       for (int q = 0; q < kScoreUnroll; ++q) {
         score_step<R, MODE, WIDE>(L, prof, cols, s0 + q, n, lane, has_above, has_below, br, bnd,
                                   dflt, OPEN, nEXT, FLOOR);
-        if constexpr (!WIDE && MODE == 0) {
-          if (stage_slot) stage_slot[q] = pack_hi16(L.botHo, L.botF);
-        }
         if constexpr (MODE == 1) {
           const int cb = s0 + q - 31;   // lane 31's column (the strip's bottom row)
           alive |= (cb >= 0) & (cb < n) & ((L.botHo > -OPEN) | (L.botF > -OPEN - nEXT));
-        }
-      }
-      if constexpr (!WIDE && MODE == 0) {
-        if (ck_col) {
-          __syncwarp();
-          if (flush_dst) flush_dst[s0 / 4] = reinterpret_cast<const uint4 *>(ck_stage)[lane];
-          __syncwarp();
-        }
-        // window boundary: state after step s0 + 7 == 32w - 1 enters window w
-        if (ck_col && ((s0 + kScoreUnroll) & 31) == 0) {
-          const int w = (s0 + kScoreUnroll) >> 5;
-          if (w < ck_nwin) {
-            uint32_t *dst = ck_col + (uint64_t)w * 32 * (R + 1);
-#pragma unroll
-            for (int r = 0; r < R; ++r) dst[32 * r] = pack_hi16(L.Ho[r], L.E[r]);
-            dst[32 * R] = pack_hi16(L.hoUpPrev, L.botF);
-          }
         }
       }
     }
@@ -510,15 +472,13 @@ __device__ __forceinline__ void load_matrix(int8_t *smat, const int8_t *mat) {
   __syncthreads();
 }
 
-template <int R, int MODE, bool WIDE, bool CKPT = false>
+template <int R, int MODE, bool WIDE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_score(KArgs A, int stage, int cls) {
   extern __shared__ __align__(16) uint8_t smem[];
   int8_t *smat = reinterpret_cast<int8_t *>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t *prof = smem + kMatBytes + warp * kProfBytes;
-  uint32_t *ck_stage = reinterpret_cast<uint32_t *>(smem + kMatBytes + kWarpsPerBlock * kProfBytes +
-                                                    warp * kStageBytes);
   load_matrix(smat, A.mat);
   const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
   int2 *bnd = A.bnd + gwarp * A.bnd_stride;
@@ -529,30 +489,9 @@ k_score(KArgs A, int stage, int cls) {
     PairState *st = A.st + k;
     if (MODE == 0) {
       const View rows{A.codes + p.a_off, 1}, cols{A.codes + p.b_off, 1};
-      uint32_t *ck = nullptr;
-      unsigned long long ck_off = 0;
-      if (CKPT) {
-        const CkLayout CL = ck_layout(R, (int)p.b_len);
-        const int nstrips = ((int)p.a_len + 32 * R - 1) / (32 * R);
-        const uint64_t bytes = (uint64_t)nstrips * CL.strip_words * 4ull;
-        if (lane == 0) ck_off = atomicAdd(A.pool_top, (unsigned long long)bytes);
-        ck_off = __shfl_sync(0xffffffffu, ck_off, 0);
-        if (ck_off + bytes <= A.pool_cap) ck = reinterpret_cast<uint32_t *>(A.pool + ck_off);
-      }
       const ScoreOut o = score_pair<R, 0, WIDE>(prof, smat, rows, cols, (int)p.a_len,
-                                                 (int)p.b_len, A.open_, A.ext, 0, bnd, lane, ck,
-                                                 ck_stage);
-      if (CKPT && lane == 0 && ck && !(o.vmax >= kScaledLimit) && (o.fwd >> 32) > 0) {
-        st->best = (int32_t)(o.fwd >> 32);
-        st->i_end = 0xFFFF - (int32_t)((o.fwd >> 16) & 0xFFFF);
-        st->j_end = 65535 - (int32_t)(o.fwd & 0xFFFF);
-        st->flags = 0;
-        st->i0 = 0;
-        st->j0 = 0;
-        st->code_off = ck_off;
-        st->box_cls = cls;
-        list_push(A, 7, cls, (uint32_t)k);
-      } else if (lane == 0) {
+                                                 (int)p.b_len, A.open_, A.ext, 0, bnd, lane);
+      if (lane == 0) {
         const int32_t best = (int32_t)(o.fwd >> 32);
         const int32_t i_end = 0xFFFF - (int32_t)((o.fwd >> 16) & 0xFFFF);
         const int32_t j_end = 65535 - (int32_t)(o.fwd & 0xFFFF);
@@ -875,6 +814,7 @@ __device__ __forceinline__ int32_t uhi(uint32_t x, int32_t B) { return (int32_t)
 
 template <int R>
 __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, const uint32_t *ck,
+                                          const uint2 *rowck, int hi,
                                           const CkLayout &CL, int strip, int g, int w, int m,
                                           int n, const RawView &acodes, const RawView &bcodes,
                                           const uint8_t *araw, const uint8_t *braw, int lane,
@@ -907,7 +847,12 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
     T.acode[q] = (uint8_t)acode;
     T.araw[q] = ra;
   }
-  const uint32_t *sbase = ck + (uint64_t)strip * CL.strip_words;
+  const uint32_t *sbase = ck + (uint64_t)strip * CL.col_words;
+  // row checkpoints of boundary b in strip st: (Ho2, F2) u16x2 words per step,
+  // this pair's half selected by `hi`
+  auto rowp = [&](int st, int b) -> const uint2 * {
+    return rowck + ((uint64_t)st * CL.row_words + (uint64_t)b * 2 * CL.spad) / 2;
+  };
   int32_t Ho = -OPEN, E = kNeg16, hoUpPrevT = -OPEN, FbotT = kNeg16;
   if (w > 0 && row_ok) {
     const uint32_t *wd = sbase + (uint64_t)w * 32 * (2 * R + 1) + tq;
@@ -929,21 +874,21 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   uint32_t topv;
   {
     int32_t tHo = -OPEN, tF = kNeg16;
-    const uint32_t *toprow = nullptr;
+    const uint2 *toprow = nullptr;
     int tsrc = 0;
     if (t0 > 0) {
-      toprow = sbase + CL.col_words + (uint64_t)ck_boundary(t0 - 1, CL) * CL.spad;
+      toprow = rowp(strip, ck_boundary(t0 - 1, CL));
       tsrc = t0 - 1;
     } else if (strip > 0) {
-      toprow = sbase - CL.strip_words + CL.col_words + (uint64_t)(CL.nb - 1) * CL.spad;
+      toprow = rowp(strip - 1, CL.nb - 1);
       tsrc = 31;
     }
     if (toprow) {
       const int idx = 32 * w - t0 + lane + tsrc;
       if (idx >= 0) {
-        const uint32_t z = toprow[idx];
-        tHo = ulo(z, B);
-        tF = uhi(z, B);
+        const uint2 z = toprow[idx];
+        tHo = (int32_t)(hi ? (z.x >> 16) : (z.x & 0xFFFFu)) - B;
+        tF = (int32_t)(hi ? (z.y >> 16) : (z.y & 0xFFFFu)) - B;
       }
     }
     T.H[0][t1 - t0 + 1 + lane] = (int16_t)(tHo + OPEN);
@@ -969,13 +914,11 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       }
       if (t2 > 0) {
         const int idx = 32 * w - t2 + lane + (t2 - 1);
-        pf(sbase + CL.col_words + (uint64_t)ck_boundary(t2 - 1, CL) * CL.spad + idx);
+        pf(rowp(strip, ck_boundary(t2 - 1, CL)) + idx);
       }
     }
     if (w > 0 && (t0 > 0 || strip > 0)) {
-      const uint32_t *row = t0 > 0 ? sbase + CL.col_words + (uint64_t)ck_boundary(t0 - 1, CL) * CL.spad
-                                   : sbase - CL.strip_words + CL.col_words +
-                                         (uint64_t)(CL.nb - 1) * CL.spad;
+      const uint2 *row = t0 > 0 ? rowp(strip, ck_boundary(t0 - 1, CL)) : rowp(strip - 1, CL.nb - 1);
       const int idx = 32 * (w - 1) - t0 + lane + (t0 > 0 ? t0 - 1 : 31);
       if (idx >= 0) pf(row + idx);
     }
@@ -1051,6 +994,8 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
   const int m = (int)p.a_len, n = (int)p.b_len;
   const CkLayout CL = ck_layout(R, st->box_n);   // layout of the forward pass's checkpoints
   const uint32_t *ck = reinterpret_cast<const uint32_t *>(A.pool + st->code_off);
+  const uint2 *rowck = reinterpret_cast<const uint2 *>(A.pool + st->code_off + st->row_delta);
+  const int hi = (st->flags & kFlagHi) ? 1 : 0;
   const uint8_t *araw = A.raw + p.a_off, *braw = A.raw + p.b_off;
   const RawView acodes{araw, A.lut}, bcodes{braw, A.lut};
   const int i_end = st->i_end;
@@ -1064,7 +1009,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
     const int best = st->best;
     const int strip = i_end / (32 * R);
     const int t = (i_end - strip * 32 * R) / R, r = i_end - strip * 32 * R - t * R;
-    const uint32_t *rmcol = ck + (uint64_t)strip * CL.strip_words + 32ull * (R + 1 + r) + t;
+    const uint32_t *rmcol = ck + (uint64_t)strip * CL.col_words + 32ull * (R + 1 + r) + t;
     int wstar = CL.nwin - 1;
     for (int w0 = 1; w0 < CL.nwin; w0 += 32) {
       const int w = w0 + lane;
@@ -1075,7 +1020,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
     }
     const int g = t / CL.G;
     const int kap_hi = min(32 * wstar - t + 31, n - 1);
-    tb_replay<R>(T, smat, ck, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+    tb_replay<R>(T, smat, ck, rowck, hi, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
                  EXT, Bias, trow0, tcmin, i_end, kap_hi);
     cs = strip; cg = g; cw = wstar;
     const int q = i_end - trow0;
@@ -1102,7 +1047,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       const int t = (rho - strip * 32 * R) / R;
       const int g = t / CL.G;
       const int w = (kap + t) >> 5;
-      tb_replay<R>(T, smat, ck, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+      tb_replay<R>(T, smat, ck, rowck, hi, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
                    EXT, Bias, trow0, tcmin, rho, kap);
       cs = strip; cg = g; cw = w;
       q = rho - trow0;
@@ -1325,7 +1270,7 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
     p = A.pairs[k];
     PairState s;
     s.best = 0; s.i_end = s.j_end = -1; s.flags = 0; s.i0 = s.j0 = 0; s.box_cls = 0;
-    s.box_n = 0; s.code_off = 0; s.box_m = 0; s.pad = 0;
+    s.box_n = 0; s.code_off = 0; s.box_m = 0; s.row_delta = 0;
     // the call's only bounds check (sw_align_batch and the device entry point):
     // a pair outside the arena or longer than 65,000 residues is never
     // scheduled; the call then fails with SW_EINVAL

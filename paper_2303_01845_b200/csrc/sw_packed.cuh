@@ -27,7 +27,7 @@
 namespace pastis {
 
 constexpr int kWarpsPerBlockP = 4;
-constexpr int kStageBytesP = 2 * 17 * 8 * 4;     // two pairs x (16 boundaries + dummy) x 8 steps
+constexpr int kStageBytesP = 17 * 8 * 8;         // (16 boundaries + dummy) x 8 steps x (Ho2, F2)
 constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs
 constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
 
@@ -132,33 +132,27 @@ __device__ __forceinline__ uint32_t sel_pair(int k) {
          ((uint32_t)((4 + k) | 8) << 12);
 }
 
-// The previous strip's bottom row comes from the row checkpoints of its
-// lane 31 (boundary nb-1), indexed by that lane's step = column + 31; both
-// pairs' words are fetched 32 columns ahead and repacked into u16x2.
+// The previous strip's bottom row comes from the duo's row checkpoints of its
+// lane 31 (boundary nb-1), indexed by that lane's step = column + 31: one
+// (Ho2, F2) pair of u16x2 words per column, fetched 32 columns ahead.
 struct PackedBoundaryReader {
-  uint32_t a_cur, b_cur, a_nxt, b_nxt;
-  const uint32_t *ra, *rb;    // row-checkpoint rows (nullptr: pair without checkpoints)
+  uint2 cur, nxt;
+  const uint2 *r;             // row-checkpoint row of the previous strip's boundary nb-1
   int n;
-  __device__ __forceinline__ uint32_t ld(const uint32_t *r, int c, uint32_t dflt) const {
-    return (r && c < n) ? r[c + 31] : dflt;
-  }
-  __device__ __forceinline__ void init(const uint32_t *ra_, const uint32_t *rb_, int n_, int lane,
-                                       uint32_t dflt) {
-    ra = ra_; rb = rb_; n = n_;
-    a_cur = ld(ra, lane, dflt); b_cur = ld(rb, lane, dflt);
-    a_nxt = ld(ra, 32 + lane, dflt); b_nxt = ld(rb, 32 + lane, dflt);
+  __device__ __forceinline__ uint2 ld(int c, uint2 dflt) const { return c < n ? r[c + 31] : dflt; }
+  __device__ __forceinline__ void init(const uint2 *r_, int n_, int lane, uint2 dflt) {
+    r = r_; n = n_;
+    cur = ld(lane, dflt);
+    nxt = ld(32 + lane, dflt);
   }
   // (Ho2, F2) for column s (lane 0's column), all lanes participate
-  __device__ __forceinline__ void get(int s, int lane, uint32_t dflt, uint32_t &ho2, uint32_t &f2) {
+  __device__ __forceinline__ void get(int s, int lane, uint2 dflt, uint32_t &ho2, uint32_t &f2) {
     if ((s & 31) == 0 && s > 0) {
-      a_cur = a_nxt; b_cur = b_nxt;
-      a_nxt = ld(ra, s + 32 + lane, dflt);
-      b_nxt = ld(rb, s + 32 + lane, dflt);
+      cur = nxt;
+      nxt = ld(s + 32 + lane, dflt);
     }
-    const uint32_t wa = __shfl_sync(0xffffffffu, a_cur, s & 31);
-    const uint32_t wb = __shfl_sync(0xffffffffu, b_cur, s & 31);
-    ho2 = prmt(wa, wb, 0x5410u);
-    f2 = prmt(wa, wb, 0x7632u);
+    ho2 = __shfl_sync(0xffffffffu, cur.x, s & 31);
+    f2 = __shfl_sync(0xffffffffu, cur.y, s & 31);
   }
 };
 
@@ -184,9 +178,8 @@ k_score_packed(KArgs A, int stage, int cls) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t *profA = smem + kMatBytes + warp * warp_bytes_p(R);
   uint8_t *profB = profA + prof_bytes_p(R);
-  uint32_t *stageA = reinterpret_cast<uint32_t *>(profB + prof_bytes_p(R));
-  uint32_t *stageB = stageA + 17 * 8;
-  uint8_t *ringA = reinterpret_cast<uint8_t *>(stageB + 17 * 8);
+  uint2 *rstage = reinterpret_cast<uint2 *>(profB + prof_bytes_p(R));   // [17][8] (Ho2, F2)
+  uint8_t *ringA = reinterpret_cast<uint8_t *>(rstage + 17 * 8);
   uint8_t *ringB = ringA + 128;
   load_matrix(smat, A.mat);
   const uint32_t Bs = (uint32_t)A.bias16;
@@ -231,26 +224,34 @@ k_score_packed(KArgs A, int stage, int cls) {
     const int m = max(P[0].m, P[1].m), n = max(P[0].n, P[1].n);
     const int nstrips = (m + 32 * R - 1) / (32 * R);
     const CkLayout CL = ck_layout(R, n);
-    const uint64_t bytes = (uint64_t)nstrips * CL.strip_words * 4ull;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (P[h].k < 0) continue;
+    // one pool allocation per duo: [pair A columns][pair B columns][duo rows]
+    const int npair = 1 + (P[1].k >= 0);
+    const uint64_t colb = (uint64_t)nstrips * CL.col_words * 4ull;
+    const uint64_t bytes = npair * colb + (uint64_t)nstrips * CL.row_words * 4ull;
+    uint2 *rowck = nullptr;
+    {
       unsigned long long off = 0;
       if (lane == 0) off = atomicAdd(A.pool_top, (unsigned long long)bytes);
       off = __shfl_sync(0xffffffffu, off, 0);
       if (off + bytes <= A.pool_cap) {
-        P[h].ck = reinterpret_cast<uint32_t *>(A.pool + off);
-        P[h].ck_off = off;
+        P[0].ck = reinterpret_cast<uint32_t *>(A.pool + off);
+        P[0].ck_off = off;
+        if (npair == 2) {
+          P[1].ck = reinterpret_cast<uint32_t *>(A.pool + off + colb);
+          P[1].ck_off = off + colb;
+        }
+        rowck = reinterpret_cast<uint2 *>(A.pool + off + npair * colb);
       }
     }
-    // The pool is one allocation carved per pair; when it is full a pair is
-    // deferred to the next round (stage 8; the pool is recycled between
-    // rounds), or -- if its checkpoints would take over a quarter of the pool
-    // -- sent to the scalar path.  A duo with no room at all skips the fill.
+    // When the pool is full the duo's pairs are deferred to the next round
+    // (stage 8; the pool is recycled between rounds), or -- a pair whose
+    // checkpoints alone would take over a quarter of the pool -- sent to the
+    // scalar path.
     auto defer = [&](int h) {
       PairState *st = A.st + P[h].k;
       const CkLayout OL = ck_layout(R, P[h].n);
-      const uint64_t own = (uint64_t)((P[h].m + 32 * R - 1) / (32 * R)) * OL.strip_words * 4ull;
+      const uint64_t own = (uint64_t)((P[h].m + 32 * R - 1) / (32 * R)) *
+                           (OL.col_words + OL.row_words) * 4ull;
       if (own > A.pool_cap / 4) {
         st->flags = 0;
         list_push(A, 0, kFallbackClass, (uint32_t)P[h].k);
@@ -259,9 +260,9 @@ k_score_packed(KArgs A, int stage, int cls) {
         list_push(A, 8, cls, (uint32_t)P[h].k);
       }
     };
-    if (!((P[0].k >= 0 && P[0].ck) || (P[1].k >= 0 && P[1].ck))) {
+    if (!rowck) {
       if (lane == 0) {
-        if (P[0].k >= 0) defer(0);
+        defer(0);
         if (P[1].k >= 0) defer(1);
       }
       continue;
@@ -292,27 +293,19 @@ k_score_packed(KArgs A, int stage, int cls) {
       auto run_strip = [&](auto above_tag) {
         constexpr bool has_above = decltype(above_tag)::value;
       PackedBoundaryReader br;
-      const uint32_t dflt = (HO0 & 0xFFFFu) | (NEG2 << 16);   // (H-open at H=0, F=-inf)
-      if (has_above) {
-        const uint64_t prev = (uint64_t)(strip - 1) * CL.strip_words + CL.col_words +
-                              (uint64_t)(CL.nb - 1) * CL.spad;
-        br.init(P[0].ck ? P[0].ck + prev : nullptr, P[1].ck ? P[1].ck + prev : nullptr, n, lane,
-                dflt);
-      }
+      const uint2 dflt = make_uint2(HO0, NEG2);   // (H-open at H=0, F=-inf), both halves
+      if (has_above)
+        br.init(rowck + ((uint64_t)(strip - 1) * CL.row_words + (uint64_t)(CL.nb - 1) * 2 * CL.spad) / 2,
+                n, lane, dflt);
       // checkpoint destinations for this strip
-      uint32_t *colA = P[0].ck ? P[0].ck + (uint64_t)strip * CL.strip_words + lane : nullptr;
-      uint32_t *colB = P[1].ck ? P[1].ck + (uint64_t)strip * CL.strip_words + lane : nullptr;
+      uint32_t *colA = P[0].ck + (uint64_t)strip * CL.col_words + lane;
+      uint32_t *colB = P[1].ck ? P[1].ck + (uint64_t)strip * CL.col_words + lane : nullptr;
       const int b = ck_boundary(lane, CL);
       const int bslot = (b >= 0 ? b : 16) * kScoreUnroll;   // non-boundary lanes -> dummy row
-      uint4 *flA = nullptr, *flB = nullptr;
-      if (lane < 2 * CL.nb) {
-        if (P[0].ck)
-          flA = reinterpret_cast<uint4 *>(P[0].ck + (uint64_t)strip * CL.strip_words + CL.col_words +
-                                          (uint32_t)(lane >> 1) * CL.spad) + (lane & 1);
-        if (P[1].ck)
-          flB = reinterpret_cast<uint4 *>(P[1].ck + (uint64_t)strip * CL.strip_words + CL.col_words +
-                                          (uint32_t)(lane >> 1) * CL.spad) + (lane & 1);
-      }
+      // row checkpoints of this strip, [boundary][step] uint2 = 16 B per two
+      // steps: lane i (and i + 32) flush 16 B chunk i of the staged 8 steps
+      uint4 *rowdst = reinterpret_cast<uint4 *>(rowck + (uint64_t)strip * CL.row_words / 2);
+      const int nchunk = CL.nb * 4;
       const int steps = n + 31;
       __syncwarp();
       for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
@@ -356,19 +349,19 @@ k_score_packed(KArgs A, int stage, int cls) {
           }
           L.botHo = L.Ho[R - 1];
           L.botF = G - OPEN2;
-          stageA[bslot + q] = prmt(L.botHo, L.botF, 0x5410u);
-          stageB[bslot + q] = prmt(L.botHo, L.botF, 0x7632u);
+          rstage[bslot + q] = make_uint2(L.botHo, L.botF);
         }
         __syncwarp();
-        if (flA) flA[s0 / 4] = reinterpret_cast<const uint4 *>(stageA)[lane];
-        if (flB) flB[s0 / 4] = reinterpret_cast<const uint4 *>(stageB)[lane];
+        for (int i = lane; i < nchunk; i += 32)   // chunk i: boundary i / 4, steps 2(i % 4) ..
+          rowdst[(uint64_t)(i >> 2) * (CL.spad / 2) + s0 / 2 + (i & 3)] =
+              reinterpret_cast<const uint4 *>(rstage)[i];
         __syncwarp();
         // column checkpoint: state entering window w (after step 32w - 1)
         if (((s0 + kScoreUnroll) & 31) == 0) {
           const int w = (s0 + kScoreUnroll) >> 5;
           if (w < CL.nwin) {
             const uint64_t base = (uint64_t)w * 32 * (2 * R + 1);
-            if (colA) {
+            {
               uint32_t *d = colA + base;
 #pragma unroll
               for (int r = 0; r < R; ++r) d[32 * r] = prmt(L.Ho[r], L.E[r], 0x5410u);
@@ -437,8 +430,9 @@ k_score_packed(KArgs A, int stage, int cls) {
           st->best = best;
           st->i_end = i_end;
           st->j_end = -1;                      // resolved by k_tb from the checkpoints
-          st->flags = kFlagNeedJ;
+          st->flags = kFlagNeedJ | (h ? kFlagHi : 0);
           st->code_off = P[h].ck_off;
+          st->row_delta = (uint32_t)((uint64_t)((const uint8_t *)rowck - A.pool) - P[h].ck_off);
           st->box_cls = cls;
           st->box_m = m;
           st->box_n = n;
