@@ -41,26 +41,25 @@ __host__ __device__ constexpr int cta_packed_warp_bytes(int R) {
   return 2 * prof_bytes_p(R) + kRingBytes;
 }
 __host__ __device__ constexpr int smem_cta_packed(int R) {
-  return kMatBytes + kCtaWarps * cta_packed_warp_bytes(R) + (int)sizeof(CtaPSync) + 16;
+  return kMatTBytes + kCtaWarps * cta_packed_warp_bytes(R) + (int)sizeof(CtaPSync) + 16;
 }
 
 template <int R>
 __global__ void __launch_bounds__(kCtaWarps * 32, 3)
 k_score_cta_packed(KArgs A, int stage, int cls) {
   extern __shared__ __align__(16) uint8_t smem[];
-  int8_t *smat = reinterpret_cast<int8_t *>(smem);
+  uint8_t *smatT = smem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t *profA = smem + kMatBytes + warp * cta_packed_warp_bytes(R);
+  uint8_t *profA = smem + kMatTBytes + warp * cta_packed_warp_bytes(R);
   uint8_t *profB = profA + prof_bytes_p(R);
   uint8_t *ringA = profB + prof_bytes_p(R);
   uint8_t *ringB = ringA + 128;
-  CtaPSync &S = *reinterpret_cast<CtaPSync *>(smem + kMatBytes + kCtaWarps * cta_packed_warp_bytes(R));
-  load_matrix(smat, A.mat);
+  CtaPSync &S = *reinterpret_cast<CtaPSync *>(smem + kMatTBytes + kCtaWarps * cta_packed_warp_bytes(R));
+  load_matrix_t(smatT, A.mat, A.prof_lo);
   uint2 *rows_ring = A.cta_rows + (uint64_t)blockIdx.x * kCtaPSlots * kCtaPRowStride;
   const uint32_t Bs = (uint32_t)A.bias16;
   const uint32_t BB = A.p_bb, OPEN2 = A.p_open2;
   const uint32_t NEG2 = A.p_ext2, HO0 = A.p_ho0, NEXT2 = A.p_next2, NOPEN2 = A.p_nopen2;
-  const int lo = A.prof_lo;
   for (;;) {
     if (threadIdx.x == 0) {
       const uint32_t pos = atomicAdd(&A.ctrs[kStages * kNumClasses + stage * kNumClasses + cls], 2u);
@@ -110,8 +109,8 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
     for (int strip = warp; strip < nstrips; strip += kCtaWarps) {
       const int row0 = strip * 32 * R;
       __syncwarp();
-      build_profile_u8<R>(profA, smat, rows0, m0, row0, lane, lo);
-      build_profile_u8<R>(profB, smat, rows1, m1, row0, lane, lo);
+      build_profile_u8<R>(profA, smatT, rows0, m0, row0, lane);
+      build_profile_u8<R>(profB, smatT, rows1, m1, row0, lane);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = -32 + 32 * q + lane;

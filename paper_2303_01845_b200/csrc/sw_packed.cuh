@@ -30,6 +30,12 @@ constexpr int kWarpsPerBlockP = 4;
 constexpr int kStageBytesP = 17 * 8 * 8;         // (16 boundaries + dummy) x 8 steps x (Ho2, F2)
 constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs
 constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
+// Profile table of the packed kernels: matT[a][code] = s(code, a) + open as
+// u8 (a = row residue, code = column residue; PAD row/column -> 0), rows
+// padded to 32 bytes so four codes load as one word.  kMatTBytes replaces
+// kMatBytes at the front of the packed kernels' shared memory.
+constexpr int kMatTStride = 32;
+constexpr int kMatTBytes = kCodes * kMatTStride + 32;
 
 // u8 profile of one pair: part 0 = [code][lane][P0] (P0 = 4 or 8 bytes),
 // part 1 = [code][lane][P1] for the remaining rows (R = 10 -> 8 + 2 bytes,
@@ -42,7 +48,7 @@ __host__ __device__ constexpr int prof_bytes_p(int R) { return kCodes * 32 * (pr
 __host__ __device__ constexpr int warp_bytes_p(int R) {
   return (2 * prof_bytes_p(R) + kStageBytesP + kRingBytes + 15) / 16 * 16;
 }
-__host__ __device__ constexpr int smem_packed(int R) { return kMatBytes + kWarpsPerBlockP * warp_bytes_p(R); }
+__host__ __device__ constexpr int smem_packed(int R) { return kMatTBytes + kWarpsPerBlockP * warp_bytes_p(R); }
 // resident blocks per SM the packed forward is compiled for (registers):
 // small R has little per-lane state, so more warps hide the latency
 #ifndef K1P_MINB_SMALL
@@ -62,35 +68,61 @@ __device__ __forceinline__ uint32_t vmax2u(uint32_t a, uint32_t b) {
 }
 __device__ __forceinline__ uint32_t splat16(uint32_t v) { return (v & 0xFFFFu) * 0x10001u; }
 
+__device__ __forceinline__ void load_matrix_t(uint8_t *matT, const int8_t *mat, int lo) {
+  for (int i = threadIdx.x; i < kMatTBytes; i += blockDim.x) {
+    const int a = i / kMatTStride, code = i % kMatTStride;
+    int v = 0;
+    if (a < kPad && code < kPad) v = (int)mat[code * kCodes + a] - lo;
+    matT[i] = (uint8_t)v;
+  }
+  __syncthreads();
+}
+
 // u8 profile (s - lo) for rows row0+lane*R .. +R-1 of one pair; PAD -> 0.
+// Four codes of one row come from one 32-bit LDS of matT; a 4x4 byte
+// transpose (8 PRMT) turns four rows x four codes into the per-code words
+// [rows 4j .. 4j+3] of the profile layout.
 template <int R, typename V>
-__device__ __forceinline__ void build_profile_u8(uint8_t *prof, const int8_t *mat, const V &rows,
-                                                 int m, int row0, int lane, int lo) {
+__device__ __forceinline__ void build_profile_u8(uint8_t *prof, const uint8_t *matT, const V &rows,
+                                                 int m, int row0, int lane) {
   constexpr int P0 = prof_p0(R), P1 = prof_p1(R);
-  int arow[R];
+  constexpr int NW = (R + 3) / 4;          // profile words per code
+  const uint8_t *rowp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int x = row0 + lane * R + r;
-    arow[r] = x < m ? rows.at(x) : kPad;
+    rowp[r] = matT + (x < m ? rows.at(x) : kPad) * kMatTStride;
   }
-#pragma unroll 2
-  for (int code = 0; code < kCodes; ++code) {
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+  for (int g = 0; g < (kCodes + 3) / 4; ++g) {
+    uint32_t W[4][NW];                      // W[k][j]: code 4g+k, rows 4j .. 4j+3
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int a = arow[r];
-      const int v = (a == kPad || code == kPad) ? 0 : (int)mat[code * kCodes + a] - lo;
-      w[r >> 2] |= (uint32_t)v << (8 * (r & 3));
+    for (int j = 0; j < NW; ++j) {
+      uint32_t v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        v[i] = 4 * j + i < R ? *reinterpret_cast<const uint32_t *>(rowp[4 * j + i] + 4 * g) : 0u;
+      const uint32_t t01l = prmt(v[0], v[1], 0x5140u), t01h = prmt(v[0], v[1], 0x7362u);
+      const uint32_t t23l = prmt(v[2], v[3], 0x5140u), t23h = prmt(v[2], v[3], 0x7362u);
+      W[0][j] = prmt(t01l, t23l, 0x5410u);
+      W[1][j] = prmt(t01l, t23l, 0x7632u);
+      W[2][j] = prmt(t01h, t23h, 0x5410u);
+      W[3][j] = prmt(t01h, t23h, 0x7632u);
     }
-    uint8_t *p0 = prof + (code * 32 + lane) * P0;
-    if (P0 == 4) *reinterpret_cast<uint32_t *>(p0) = w[0];
-    else *reinterpret_cast<uint2 *>(p0) = make_uint2(w[0], w[1]);
-    if (P1 > 0) {
-      constexpr int k1 = P0 / 4;       // first word of part 1
-      uint8_t *p1 = prof + kCodes * 32 * P0 + (code * 32 + lane) * P1;
-      if (P1 == 2) *reinterpret_cast<uint16_t *>(p1) = (uint16_t)w[k1];
-      else if (P1 == 4) *reinterpret_cast<uint32_t *>(p1) = w[k1];
-      else *reinterpret_cast<uint2 *>(p1) = make_uint2(w[k1], w[k1 + 1]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int code = 4 * g + k;
+      if (code >= kCodes) break;
+      uint8_t *p0 = prof + (code * 32 + lane) * P0;
+      if (P0 == 4) *reinterpret_cast<uint32_t *>(p0) = W[k][0];
+      else *reinterpret_cast<uint2 *>(p0) = make_uint2(W[k][0], W[k][1]);
+      if (P1 > 0) {
+        constexpr int k1 = P0 / 4;       // first word of part 1
+        uint8_t *p1 = prof + kCodes * 32 * P0 + (code * 32 + lane) * P1;
+        if (P1 == 2) *reinterpret_cast<uint16_t *>(p1) = (uint16_t)W[k][k1];
+        else if (P1 == 4) *reinterpret_cast<uint32_t *>(p1) = W[k][k1];
+        else *reinterpret_cast<uint2 *>(p1) = make_uint2(W[k][k1], W[k][k1 + 1]);
+      }
     }
   }
 }
@@ -174,21 +206,20 @@ template <int R>
 __global__ void __launch_bounds__(kWarpsPerBlockP * 32, packed_min_blocks(R))
 k_score_packed(KArgs A, int stage, int cls) {
   extern __shared__ __align__(16) uint8_t smem[];
-  int8_t *smat = reinterpret_cast<int8_t *>(smem);
+  uint8_t *smatT = smem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t *profA = smem + kMatBytes + warp * warp_bytes_p(R);
+  uint8_t *profA = smem + kMatTBytes + warp * warp_bytes_p(R);
   uint8_t *profB = profA + prof_bytes_p(R);
   uint2 *rstage = reinterpret_cast<uint2 *>(profB + prof_bytes_p(R));   // [17][8] (Ho2, F2)
   uint8_t *ringA = reinterpret_cast<uint8_t *>(rstage + 17 * 8);
   uint8_t *ringB = ringA + 128;
-  load_matrix(smat, A.mat);
+  load_matrix_t(smatT, A.mat, A.prof_lo);
   const uint32_t Bs = (uint32_t)A.bias16;
   const uint32_t BB = A.p_bb;
   const uint32_t OPEN2 = A.p_open2;
   const uint32_t NEG2 = A.p_ext2;                      // biased "-inf": E/F - ext == 0
   const uint32_t HO0 = A.p_ho0;                        // biased H - open for H == 0
   const uint32_t NEXT2 = A.p_next2, NOPEN2 = A.p_nopen2;  // per-half -ext, -open
-  const int lo = A.prof_lo;
   for (;;) {
     // two consecutive work items per warp
     uint32_t pos = 0;
@@ -272,8 +303,8 @@ k_score_packed(KArgs A, int stage, int cls) {
     for (int strip = 0; strip < nstrips; ++strip) {
       const int row0 = strip * 32 * R;
       __syncwarp();
-      build_profile_u8<R>(profA, smat, P[0].rows, P[0].m, row0, lane, lo);
-      build_profile_u8<R>(profB, smat, P[1].rows, P[1].m, row0, lane, lo);
+      build_profile_u8<R>(profA, smatT, P[0].rows, P[0].m, row0, lane);
+      build_profile_u8<R>(profB, smatT, P[1].rows, P[1].m, row0, lane);
       __syncwarp();
       PackedLane<R> L;
 #pragma unroll
