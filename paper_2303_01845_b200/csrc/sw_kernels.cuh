@@ -826,14 +826,6 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   const int cmin = 32 * w - t1;              // tile column index x = c - cmin + 1
   const int width = 32 + (t1 - t0);
   tcmin = cmin;
-  __syncwarp();
-  for (int x = lane; x < width; x += 32) {
-    const int c = cmin + x;
-    const bool ok = (c >= 0) & (c < n);
-    const uint8_t rb = ok ? __ldcg(braw + c) : (uint8_t)0;
-    T.bcode[x] = ok ? (uint8_t)__ldg(bcodes.lut + rb) : (uint8_t)kPad;
-    T.braw[x] = rb;
-  }
   // the walk enters at (rho_in, kap_in) and only moves up/left
   const int qmax = rho_in - trow0;
   const int q = lane;
@@ -841,26 +833,60 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   const int tq = t0 + q / R, rq = q - (q / R) * R;
   const int rho = trow0 + q;
   const bool real_row = row_ok & (rho < m);
-  const uint8_t ra = real_row ? __ldcg(araw + rho) : (uint8_t)0;
-  const int acode = real_row ? (int)__ldg(acodes.lut + ra) : kPad;
-  if (row_ok) {
-    T.acode[q] = (uint8_t)acode;
-    T.araw[q] = ra;
-  }
   const uint32_t *sbase = ck + (uint64_t)strip * CL.col_words;
   // row checkpoints of boundary b in strip st: (Ho2, F2) u16x2 words per step,
   // this pair's half selected by `hi`
   auto rowp = [&](int st, int b) -> const uint2 * {
     return rowck + ((uint64_t)st * CL.row_words + (uint64_t)b * 2 * CL.spad) / 2;
   };
-  int32_t Ho = -OPEN, E = kNeg16, hoUpPrevT = -OPEN, FbotT = kNeg16;
-  if (w > 0 && row_ok) {
+  // Issue every global load of the set-up first (residue bytes of the tile's
+  // columns and rows, this row's column checkpoint, the top halo row) so their
+  // latencies overlap, then the LUT lookups, then the shared-memory stores.
+  const int c0 = cmin + lane, c1 = cmin + 32 + lane;
+  const bool ok0 = (c0 >= 0) & (c0 < n), ok1 = (32 + lane < width) & (c1 >= 0) & (c1 < n);
+  const uint8_t rb0 = ok0 ? __ldcg(braw + c0) : (uint8_t)0;
+  const uint8_t rb1 = ok1 ? __ldcg(braw + c1) : (uint8_t)0;
+  const uint8_t ra = real_row ? __ldcg(araw + rho) : (uint8_t)0;
+  uint32_t ckx = 0u, cky = 0u;
+  const bool have_ck = (w > 0) & row_ok;
+  if (have_ck) {
     const uint32_t *wd = sbase + (uint64_t)w * 32 * (2 * R + 1) + tq;
-    const uint32_t x = wd[32 * rq], y = wd[32 * R];
-    Ho = ulo(x, B);
-    E = uhi(x, B);
-    hoUpPrevT = ulo(y, B);
-    FbotT = uhi(y, B);
+    ckx = wd[32 * rq];
+    cky = wd[32 * R];
+  }
+  const uint2 *toprow = nullptr;
+  int tsrc = 0;
+  if (t0 > 0) {
+    toprow = rowp(strip, ck_boundary(t0 - 1, CL));
+    tsrc = t0 - 1;
+  } else if (strip > 0) {
+    toprow = rowp(strip - 1, CL.nb - 1);
+    tsrc = 31;
+  }
+  const int tidx = 32 * w - t0 + lane + tsrc;
+  const bool have_top = toprow && tidx >= 0;
+  uint2 z = make_uint2(0u, 0u);
+  if (have_top) z = toprow[tidx];
+  const uint8_t bc0 = ok0 ? (uint8_t)__ldg(bcodes.lut + rb0) : (uint8_t)kPad;
+  const uint8_t bc1 = ok1 ? (uint8_t)__ldg(bcodes.lut + rb1) : (uint8_t)kPad;
+  const int acode = real_row ? (int)__ldg(acodes.lut + ra) : kPad;
+  __syncwarp();
+  T.bcode[lane] = bc0;
+  T.braw[lane] = rb0;
+  if (32 + lane < width) {
+    T.bcode[32 + lane] = bc1;
+    T.braw[32 + lane] = rb1;
+  }
+  if (row_ok) {
+    T.acode[q] = (uint8_t)acode;
+    T.araw[q] = ra;
+  }
+  int32_t Ho = -OPEN, E = kNeg16, hoUpPrevT = -OPEN, FbotT = kNeg16;
+  if (have_ck) {
+    Ho = ulo(ckx, B);
+    E = uhi(ckx, B);
+    hoUpPrevT = ulo(cky, B);
+    FbotT = uhi(cky, B);
   }
   // halo: this row's left boundary (column c_lo - 1) and, for the first row of
   // each forward lane, the diagonal above it (column c_lo - 1 of the row above)
@@ -874,22 +900,9 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   uint32_t topv;
   {
     int32_t tHo = -OPEN, tF = kNeg16;
-    const uint2 *toprow = nullptr;
-    int tsrc = 0;
-    if (t0 > 0) {
-      toprow = rowp(strip, ck_boundary(t0 - 1, CL));
-      tsrc = t0 - 1;
-    } else if (strip > 0) {
-      toprow = rowp(strip - 1, CL.nb - 1);
-      tsrc = 31;
-    }
-    if (toprow) {
-      const int idx = 32 * w - t0 + lane + tsrc;
-      if (idx >= 0) {
-        const uint2 z = toprow[idx];
-        tHo = (int32_t)(hi ? (z.x >> 16) : (z.x & 0xFFFFu)) - B;
-        tF = (int32_t)(hi ? (z.y >> 16) : (z.y & 0xFFFFu)) - B;
-      }
+    if (have_top) {
+      tHo = (int32_t)(hi ? (z.x >> 16) : (z.x & 0xFFFFu)) - B;
+      tF = (int32_t)(hi ? (z.y >> 16) : (z.y & 0xFFFFu)) - B;
     }
     T.H[0][t1 - t0 + 1 + lane] = (int16_t)(tHo + OPEN);
     topv = ((uint32_t)tHo & 0xFFFFu) | ((uint32_t)tF << 16);
