@@ -813,7 +813,8 @@ __device__ __forceinline__ int32_t ulo(uint32_t x, int32_t B) { return (int32_t)
 __device__ __forceinline__ int32_t uhi(uint32_t x, int32_t B) { return (int32_t)(x >> 16) - B; }
 
 template <int R>
-__device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, const uint32_t *ck,
+__device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, const uint8_t *slut,
+                                          const uint32_t *ck,
                                           const uint2 *rowck, int hi,
                                           const CkLayout &CL, int strip, int g, int w, int m,
                                           int n, const RawView &acodes, const RawView &bcodes,
@@ -867,9 +868,9 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   const bool have_top = toprow && tidx >= 0;
   uint2 z = make_uint2(0u, 0u);
   if (have_top) z = toprow[tidx];
-  const uint8_t bc0 = ok0 ? (uint8_t)__ldg(bcodes.lut + rb0) : (uint8_t)kPad;
-  const uint8_t bc1 = ok1 ? (uint8_t)__ldg(bcodes.lut + rb1) : (uint8_t)kPad;
-  const int acode = real_row ? (int)__ldg(acodes.lut + ra) : kPad;
+  const uint8_t bc0 = ok0 ? slut[rb0] : (uint8_t)kPad;   // shared-memory LUT
+  const uint8_t bc1 = ok1 ? slut[rb1] : (uint8_t)kPad;
+  const int acode = real_row ? (int)slut[ra] : kPad;
   __syncwarp();
   T.bcode[lane] = bc0;
   T.braw[lane] = rb0;
@@ -1000,7 +1001,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
 // (PairState: best, i_end, code_off, box_n, flags & kFlagNeedJ); one warp.
 template <int R>
 __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8_t *smat,
-                                        int64_t k, int lane) {
+                                        const uint8_t *slut, int64_t k, int lane) {
   const int32_t OPEN = A.open_, EXT = A.ext, Bias = A.bias16;
   const sw_pair_t p = A.pairs[k];
   PairState *st = A.st + k;
@@ -1033,7 +1034,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
     }
     const int g = t / CL.G;
     const int kap_hi = min(32 * wstar - t + 31, n - 1);
-    tb_replay<R>(T, smat, ck, rowck, hi, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+    tb_replay<R>(T, smat, slut, ck, rowck, hi, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
                  EXT, Bias, trow0, tcmin, i_end, kap_hi);
     cs = strip; cg = g; cw = wstar;
     const int q = i_end - trow0;
@@ -1060,7 +1061,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       const int t = (rho - strip * 32 * R) / R;
       const int g = t / CL.G;
       const int w = (kap + t) >> 5;
-      tb_replay<R>(T, smat, ck, rowck, hi, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+      tb_replay<R>(T, smat, slut, ck, rowck, hi, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
                    EXT, Bias, trow0, tcmin, rho, kap);
       cs = strip; cg = g; cw = w;
       q = rho - trow0;
@@ -1147,17 +1148,19 @@ k_tb(KArgs A, int stage, int cls) {
   struct Shared {
     TbSmem<R> t[kTbWarps];
     int8_t mat[kCodes * kCodes];
+    uint8_t lut[256];                   // raw byte -> residue code
   };
   __shared__ __align__(16) Shared sh;   // one shared window base for tiles and matrix
   int8_t *smat = sh.mat;
   for (int i = threadIdx.x; i < kCodes * kCodes; i += blockDim.x) smat[i] = A.mat[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.lut[i] = A.lut[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   TbSmem<R> &T = sh.t[warp];
   for (;;) {
     const int64_t k = next_item(A, stage, cls, lane);
     if (k < 0) break;
-    tb_pair<R>(A, T, smat, k, lane);
+    tb_pair<R>(A, T, smat, sh.lut, k, lane);
   }
 }
 
