@@ -424,6 +424,14 @@ def main():
                                    "cell (4 adds + 5 maxes); pipe rates measured in tools/microbench",
                      "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 32/(m*n) = 0.0070 B "
                                  "-> non-binding (HBM would allow ~9e14 CUPS)",
+                     # context for `frac`: the ALU-pipe ceiling of the cell as written
+                     # (PRMT 2 + 3 VIADDMNMX 6 + VIMNMX3 2 + VIMNMX 1 = 11 ALU-pipe
+                     # cycles per packed row-word; ncu shows that pipe at 74 %), and the
+                     # cells the kernel computes per algorithmic cell (strip padding
+                     # 320/300 rows x wavefront skew (n+31)/n steps at config 2)
+                     "alu_pipe_ceiling": sms * clk_ghz * 4 * 64 / 11.0,
+                     "computed_cells_per_cell": (320 * 331) / (300 * 300)
+                     if args.workload == "config2" else None,
                      **traffic_fields(fwd_ms, args)},
         "e2e": {"value": e2e_value, "unit": "GCUPS",
                 "h2d_bytes_per_step": int(arena_np.size + table_np.nbytes),
