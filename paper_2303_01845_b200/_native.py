@@ -32,7 +32,7 @@ RESULT_DTYPE = np.dtype(
 assert PAIR_DTYPE.itemsize == 24 and RESULT_DTYPE.itemsize == 32
 
 SW_OK, SW_EINVAL, SW_ECUDA, SW_EINTERNAL, SW_EFORMAT, SW_ERANGE = 0, -1, -2, -3, -4, -5
-STATUS_OK, STATUS_EMPTY, STATUS_INTERNAL = 0, 1, 2
+STATUS_OK, STATUS_EMPTY, STATUS_INTERNAL, STATUS_INVALID = 0, 1, 2, 3  # SW_STATUS_* (include/pastis_sw.h)
 
 # every symbol include/pastis_sw.h declares
 EXPORTED_SYMBOLS = (

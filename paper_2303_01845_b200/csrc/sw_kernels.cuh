@@ -263,8 +263,9 @@ struct BoundaryReader {
 //    as biased u16 (v + B);
 //  * row checkpoints: "boundary" lanes (the last lane of each group of
 //    G = 32/R lanes, and lane 31) store their bottom-row (Ho, F) every step.
-// Per strip: [window][word (R+1)][lane] words (coalesced stores), then
-// [boundary][step] words.
+// Per strip: [window][word 0..2R][lane] words per pair (coalesced stores), and
+// [boundary][step][2] words per duo -- the raw (Ho2, F2) u16x2 words of the
+// packed pass, both pairs in one word (PairState.row_delta, kFlagHi).
 // ---------------------------------------------------------------------------
 struct CkLayout {
   int G, nb, nwin, spad;

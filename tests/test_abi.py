@@ -85,3 +85,14 @@ def test_param_domain_checked_before_device():
         _native.align_host(arena, t, _native.make_params(11, 1, m))
     with pytest.raises(ValueError, match="gap_open >= gap_extend"):
         _native.align_host(arena, t, _native.make_params(1, 2, np.zeros((25, 25), np.int32)))
+
+
+def test_status_and_return_codes_match_the_header():
+    """The Python mirror's SW_* return codes and SW_STATUS_* record statuses are
+    the header's #defines."""
+    src = open(HEADER).read()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+(SW_[A-Z_]+)\s+\(?(-?\d+)\)?", src)}
+    for name in ("OK", "EMPTY", "INTERNAL", "INVALID"):
+        assert getattr(_native, f"STATUS_{name}") == defs[f"SW_STATUS_{name}"], name
+    for name in ("SW_OK", "SW_EINVAL", "SW_ECUDA", "SW_EINTERNAL"):
+        assert getattr(_native, name) == defs[name], name
