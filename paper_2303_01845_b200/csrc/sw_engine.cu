@@ -959,7 +959,8 @@ int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena
   };
   for (uint64_t k = 0; k < n_pairs; ++k) {
     const sw_pair_t &p = pairs[k];
-    if (p.a_off + p.a_len > arena_bytes || p.b_off + p.b_len > arena_bytes)
+    if (p.a_off > arena_bytes || p.a_len > arena_bytes - p.a_off || p.b_off > arena_bytes ||
+        p.b_len > arena_bytes - p.b_off)
       return fail(SW_EINVAL, "pair references bytes outside the arena");   // before any read
     Shard &S = sh[shard[k]];
     sw_pair_t q = p;

@@ -1291,7 +1291,8 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
     // the call's only bounds check (sw_align_batch and the device entry point):
     // a pair outside the arena or longer than 65,000 residues is never
     // scheduled; the call then fails with SW_EINVAL
-    if (p.a_off + p.a_len > A.arena_bytes || p.b_off + p.b_len > A.arena_bytes ||
+    if (p.a_off > A.arena_bytes || p.a_len > A.arena_bytes - p.a_off ||   // no u64 wrap
+        p.b_off > A.arena_bytes || p.b_len > A.arena_bytes - p.b_off ||
         p.a_len > 65000u || p.b_len > 65000u) {
       s.flags = kFlagInvalid;
       atomicAdd(&stats[5], 1ull);

@@ -163,6 +163,10 @@ def test_invalid_pairs_fail_the_call_and_the_next_call_is_exact():
     bad["b_off"][7] = arena.size          # one byte past the end
     with pytest.raises(ValueError, match="outside the arena"):
         _native.align_host(arena, bad, p)
+    wrap = table.copy()
+    wrap["a_off"][5] = np.uint64(2**64 - 8)   # offset + length wraps around u64
+    with pytest.raises(ValueError, match="outside the arena"):
+        _native.align_host(arena, wrap, p)
     long = table.copy()
     long["a_len"][3] = 65001
     with pytest.raises(ValueError):
