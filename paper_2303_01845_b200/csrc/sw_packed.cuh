@@ -27,6 +27,10 @@
 namespace pastis {
 
 constexpr int kWarpsPerBlockP = 4;
+#ifndef K1P_PROF_UNROLL
+#define K1P_PROF_UNROLL 7
+#endif
+constexpr int kProfUnroll = K1P_PROF_UNROLL;   // code groups per profile-build iteration
 constexpr int kStageBytesP = 17 * 8 * 8;         // (16 boundaries + dummy) x 8 steps x (Ho2, F2)
 constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs
 constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
@@ -93,7 +97,7 @@ __device__ __forceinline__ void build_profile_u8(uint8_t *prof, const uint8_t *m
     const int x = row0 + lane * R + r;
     rowp[r] = matT + (x < m ? rows.at(x) : kPad) * kMatTStride;
   }
-#pragma unroll 1
+#pragma unroll kProfUnroll
   for (int g = 0; g < (kCodes + 3) / 4; ++g) {
     uint32_t W[4][NW];                      // W[k][j]: code 4g+k, rows 4j .. 4j+3
 #pragma unroll
