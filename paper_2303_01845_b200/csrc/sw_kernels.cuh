@@ -804,7 +804,7 @@ struct TbSmem {
   static constexpr int kRows = G * R + 1;
   static constexpr int kX = (G + 32 + 1) / 2 * 2;
   int16_t H[kRows][kX], E[kRows][kX], F[kRows][kX];  // row 0 / col 0 = halo
-  uint4 row[32];        // per tile row: (Ho, E) and (diag above, F_bot) at c_lo - 1, matrix row
+  int4 row[32];         // per tile row: E at c_lo, H at c_lo - 1, matrix row, diag above / F_bot
   uint8_t bcode[kX], braw[kX];
   uint8_t acode[32], araw[32];
 };
@@ -950,9 +950,11 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   // forward lane shifts the columns left by one, so the row above is shifted
   // one lane up; its lane-0 cell and the diagonal come from the checkpoints.
   if (row_ok)
-    T.row[q] = make_uint4(((uint32_t)Ho & 0xFFFFu) | ((uint32_t)E << 16),
-                          ((uint32_t)hoUpPrevT & 0xFFFFu) | ((uint32_t)FbotT << 16),
-                          (uint32_t)(acode * kCodes), 0u);
+    T.row[q] = make_int4(max(E - EXT, Ho),         // E at c_lo (left boundary)
+                         Ho + OPEN,                 // H at c_lo - 1
+                         acode * kCodes,            // matrix row of the residue
+                         rq == 0 ? hoUpPrevT + OPEN // first row: the diagonal above c_lo - 1
+                                 : FbotT);          // (last row: F at c_lo - 1)
   int32_t upH = (int32_t)(int16_t)(topv & 0xFFFFu) + OPEN, upF = (int32_t)topv >> 16;
   int32_t prevHb = 0, prevFb = kNeg16;   // H / F of the previous row at ITS c_lo - 1
   const int32_t Kl = (lane + 1) * EXT - OPEN, lext = lane * EXT;
@@ -970,10 +972,9 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (qq > qmax) break;
-      const uint4 rw = T.row[qq];            // broadcast
-      const int32_t HbO = (int32_t)(int16_t)(rw.x & 0xFFFFu), Eb = (int32_t)rw.x >> 16;
+      const int4 rw = T.row[qq];             // broadcast
       int32_t dg = __shfl_up_sync(0xffffffffu, upH, 1);
-      if (lane == 0) dg = r == 0 ? (int32_t)(int16_t)(rw.y & 0xFFFFu) + OPEN : prevHb;
+      if (lane == 0) dg = r == 0 ? rw.w : prevHb;
       const int32_t sc = mcol[rw.z];
       const int32_t f = max(upF - EXT, upH - OPEN);
       const int32_t ht = __vimax3_s32_relu(dg + sc, f, 0);
@@ -981,7 +982,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) z = max(z, (int32_t)__shfl_up_sync(0xffffffffu, z, d));
       int32_t ex = __shfl_up_sync(0xffffffffu, z, 1);
-      const int32_t x0e = max(Eb - EXT, HbO);               // E at c_lo (left boundary)
+      const int32_t x0e = rw.x;                             // E at c_lo (left boundary)
       if (lane == 0) ex = x0e;
       const int32_t e = max(x0e, ex) - lext;
       const int32_t h = max(ht, e);
@@ -990,8 +991,8 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       T.F[qq + 1][xs] = (int16_t)f;
       upH = h;
       upF = f;
-      prevHb = HbO + OPEN;
-      prevFb = (int32_t)rw.y >> 16;
+      prevHb = rw.y;
+      prevFb = rw.w;                         // used after the forward lane's last row
       ++qq;
     }
   }
