@@ -1,21 +1,29 @@
 """Benchmark of the alignment stage (BASELINE.json metric: SW GCUPS and
-alignments/s on B200 vs the reference CPU aligner).
+alignments/s on B200 vs the reference CPU aligner on the host cores).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload config3|config2|config5]
 
-Workload (BASELINE.json configs[1] = "config 2"): per GPU, 100,000 synthetic
-300x300 protein pairs (50% homologs with substitutions + indels), BLOSUM62,
-gap 11/1.  One step = the full hot path over that batch: forward score +
-end cell, reverse pass, box traceback -> all AlignmentResult fields.
-  value : GCUPS with inputs resident in HBM (device C-ABI entry point),
-          device time from CUDA events on the launching stream, L2 flushed
-          between steps, max over ranks.
-  e2e   : the same metric through the host C-ABI call (sw_align_batch):
-          pinned host arena + pair table in, host results out, copies timed.
-N>1 runs one process per GPU under torchrun (weak scaling: every rank aligns
-its own 100k-pair shard); no collective on the data path, only the timing
-reductions.  --impl reference times the reference algorithm (the numpy
-restatement of align.py, forked process lanes, all host cores) instead.
+Workload (default): BASELINE.json configs[2] = "config 3", the largest
+single-GPU pair batch: 1,000,000 synthetic protein pairs per GPU with
+Metaclust-like skewed lengths (len(a) ~ clip(LogNormal(5.5, 0.75), 30, 2000);
+half the b's length-correlated homologs with 30 % substitutions + 8 % indels,
+half independent draws), BLOSUM62, gap 11/1 (pastis_synth/gen.c, seeded).
+One step = the full hot path over that batch: forward score + end cell,
+traceback (tile replay / reverse pass + box) -> every AlignmentResult field.
+  value   : GCUPS (sum of |a||b| per second) with inputs resident in HBM
+            (device C-ABI entry point), CUDA events on the launching stream,
+            L2 flushed between steps, max over ranks.
+  e2e     : the same metric through the host C-ABI call (sw_align_batch):
+            pinned host arena + pair table in, host result records out, the
+            copies inside the timed region.
+  api_e2e : the same through the reference-shaped Python API
+            (AlignEngine.submit(list[(str, str, payload)]).result()), with
+            host packing and result materialisation reported separately.
+N>1 runs one process per GPU under torchrun (weak scaling: N x 1M pairs).
+--impl reference times the reference algorithm (the numpy restatement of
+align.py:79-181 in forked lanes over all host cores) on bounded samples of
+the same batch.
 """
 
 import argparse
@@ -32,33 +40,47 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = "config2"
-# BASELINE.json configs: 2 = 100k 300x300 pairs, 3 = 1M skewed-length pairs,
-# 5 = 10k long pairs (2,000-35,000 aa)
-DEFAULT_PAIRS = {"config2": 100_000, "config3": 1_000_000, "config5": 10_000}
-LENGTH = 300
 GAP = (11, 1)
-METRIC = "SW GCUPS (config 2: 300x300 pairs, BLOSUM62, gap 11/1; full alignment incl. traceback)"
+WORKLOADS = {
+    "config3": {"pairs": 1_000_000,
+                "desc": "config 3: 1M pairs/GPU, skewed lengths 30-2000 (lognormal, median 245), "
+                        "50% homologs, BLOSUM62, gap 11/1",
+                "cpu_sample": 24_000, "ref_sample": 3_000},
+    "config2": {"pairs": 100_000,
+                "desc": "config 2: 100k pairs/GPU of 300x300, 50% homologs, BLOSUM62, gap 11/1",
+                "cpu_sample": 64_000, "ref_sample": 4_000},
+    "config5": {"pairs": 10_000,
+                "desc": "config 5: 10k pairs/GPU, lengths U[2000, 35000] (independent), "
+                        "BLOSUM62, gap 11/1",
+                "cpu_sample": 24, "ref_sample": 2},
+}
+DTYPE = "int16x2 (biased u16x2 DPX lanes, exact; int32 re-run on overflow)"
+
+
+def metric_of(workload: str) -> str:
+    return ("SW GCUPS, full alignment incl. traceback (" + WORKLOADS[workload]["desc"] + ")")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
     ap.add_argument("--pairs", type=int, default=None,
                     help="pairs per GPU (default: the BASELINE config's count)")
-    ap.add_argument("--cpu-sample", type=int, default=64000,
-                    help="pairs in the bounded CPU-baseline sample (~12 s on 16 cores)")
-    ap.add_argument("--ref-sample", type=int, default=4000,
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="pairs in the bounded CPU-baseline sample (~10-20 s of host CPU)")
+    ap.add_argument("--ref-sample", type=int, default=None,
                     help="pairs per step of --impl reference (bounded sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default=WORKLOAD, choices=["config2", "config3", "config5"],
-                    help="exploration only; the headline bench is config2")
+    ap.add_argument("--no-api", action="store_true", help="skip the Python-API e2e leg")
     args = ap.parse_args()
-    if args.pairs is None:
-        args.pairs = DEFAULT_PAIRS[args.workload]
+    w = WORKLOADS[args.workload]
+    args.pairs = args.pairs or w["pairs"]
+    args.cpu_sample = args.cpu_sample or w["cpu_sample"]
+    args.ref_sample = args.ref_sample or w["ref_sample"]
     return args
 
 
@@ -69,11 +91,11 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_bench(mode: str, pairs: int, seed: int = 2303) -> dict:
+def cpu_bench(mode: str, workload: str, pairs: int, seed: int = 2303, offset: int = 0) -> dict:
     """Run oracle/cpu_bench.py in a fresh process (it forks worker lanes)."""
-    cmd = [sys.executable, "-m", "oracle.cpu_bench", "--mode", mode, "--workload", WORKLOAD,
-           "--pairs", str(pairs), "--seed", str(seed), "--gap-open", str(GAP[0]),
-           "--gap-extend", str(GAP[1])]
+    cmd = [sys.executable, "-m", "oracle.cpu_bench", "--mode", mode, "--workload", workload,
+           "--pairs", str(pairs), "--seed", str(seed), "--offset", str(offset),
+           "--gap-open", str(GAP[0]), "--gap-extend", str(GAP[1])]
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, check=True)
     return json.loads(out.stdout.strip().splitlines()[-1])
 
@@ -168,70 +190,125 @@ class ClockSampler:
                 "window": "timed region" if inside else "whole run (no sample inside the timed region)"}
 
 
-def traffic_fields(fwd_ms, args) -> dict:
-    """roofline.traffic: DRAM bytes per K1p launch from the committed ncu
-    --set full capture (profiles/r01/k1p_traffic.json), beside the algorithmic
-    bytes, and the HBM fraction they imply at this run's forward time against
-    MEASURED_PEAKS.json's copy bandwidth."""
-    out = {"traffic": None}
-    if args.workload != "config2" or args.pairs != DEFAULT_PAIRS["config2"]:
-        return out      # the capture is of the default configuration
+
+
+# --- roofline context -------------------------------------------------------
+CLASS_ROWS = (4, 6, 7, 8, 9, 10, 16)      # sw_kernels.cuh class_rows()
+FUSED_MAX_CELLS = 1 << 22                 # kFusedMaxCells: the packed (K1p) pairs
+
+
+def packed_class_of(m: np.ndarray, n: np.ndarray) -> np.ndarray:
+    """Vectorised sw_kernels.cuh packed_class_of (issue-slot cost model)."""
+    costs = []
+    for R in CLASS_ROWS:
+        S = (m + 32 * R - 1) // (32 * R)
+        c = S * (n + 31) * (9 * R + 23) + (S - 1) * (n + 31) * 6 + S * 260 * R
+        costs.append(c * (1.5 if R >= 12 else 1.0))
+    return np.argmin(np.stack(costs), axis=0)
+
+
+def computed_cells(table) -> dict:
+    """Cells K1p computes per algorithmic cell for this batch: each work list
+    (class) is sorted by shape (m, n descending) and consumed two pairs per
+    warp; a duo computes strips(max m) x 32R rows x (max n + 31) wavefront
+    steps in both u16 halves."""
+    m = table["a_len"].astype(np.int64)
+    n = table["b_len"].astype(np.int64)
+    cells = m * n
+    k1p = (cells > 0) & (cells <= FUSED_MAX_CELLS)
+    if not k1p.any():
+        return {"computed_cells_per_cell": None, "k1p_cell_fraction": 0.0}
+    m, n = m[k1p], n[k1p]
+    cls = packed_class_of(m, n)
+    order = np.lexsort((np.arange(len(m)), -n, -m, cls))
+    m, n, cls = m[order], n[order], cls[order]
+    comp = 0
+    for c, R in enumerate(CLASS_ROWS):
+        sel = cls == c
+        if not sel.any():
+            continue
+        mc, nc = m[sel], n[sel]
+        if len(mc) % 2:
+            mc, nc = np.append(mc, 0), np.append(nc, 0)
+        md = np.maximum(mc[0::2], mc[1::2])
+        nd = np.maximum(nc[0::2], nc[1::2])
+        rows = (md + 32 * R - 1) // (32 * R) * 32 * R
+        comp += int((rows * (nd + 31)).sum()) * 2
+    alg = int((table["a_len"].astype(np.int64) * table["b_len"].astype(np.int64))[k1p].sum())
+    tot = int((table["a_len"].astype(np.int64) * table["b_len"].astype(np.int64)).sum())
+    return {"computed_cells_per_cell": comp / alg, "k1p_cell_fraction": alg / tot}
+
+
+def ncu_fields(workload: str, per_step_ms: float) -> dict:
+    """roofline.traffic and the kernel shares of the step from the committed
+    ncu captures of this configuration (profiles/r02/ncu_<workload>.json,
+    written by tools/ncu_summary.py from `ncu --set full` and the
+    gpu__time_duration launch list)."""
+    path = os.path.join(ROOT, "profiles", "r02", f"ncu_{workload}.json")
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "k1p_traffic.json")) as fh:
+        with open(path) as fh:
             t = json.load(fh)
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            hbm = float(json.load(fh)["hbm_gbs"])
-    except (OSError, KeyError, ValueError):
-        return out
-    per_launch_s = float(np.mean(fwd_ms)) / 1e3 if len(fwd_ms) else 0.0
-    out["traffic"] = t["traffic_bytes_per_launch"]
-    out["traffic_unit"] = "bytes per K1p launch (config 2, 100k pairs; ncu dram__bytes_read+write)"
-    out["algorithmic_bytes_per_launch"] = t["algorithmic_bytes_per_launch"]
-    out["traffic_note"] = t["note"]
-    if per_launch_s > 0:
-        out["hbm_gbs_at_traffic"] = t["traffic_bytes_per_launch"] / per_launch_s / 1e9
-        out["hbm_frac"] = out["hbm_gbs_at_traffic"] / hbm
-        out["hbm_peak_gbs"] = hbm
+    except (OSError, ValueError):
+        return {"traffic": None, "traffic_note": f"no committed capture ({path})"}
+    out = {"traffic": t.get("traffic_bytes_per_launch"),
+           "traffic_unit": "DRAM bytes per launch of the dominant kernel (ncu dram__bytes_read.sum"
+                           " + dram__bytes_write.sum, --set full)",
+           "algorithmic_bytes_per_launch": t.get("algorithmic_bytes_per_launch"),
+           "traffic_note": t.get("note"),
+           "kernel_share_ncu": t.get("kernel_share")}
     return out
 
 
+# --- reference arm ----------------------------------------------------------
 def run_reference(args, rank: int, world: int) -> None:
-    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    """--impl reference: the reference algorithm on the host cores (rank 0 only),
+    each step a bounded sample (consecutive slices) of the batch our arm times."""
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
-    vals = []
+    vals, secs, alns = [], [], []
     last = None
     for step in range(args.warmup + args.steps):
-        r = cpu_bench("numpy", args.ref_sample, seed=2303 + step)
+        r = cpu_bench("numpy", args.workload, args.ref_sample, seed=2303,
+                      offset=step * args.ref_sample)
         if step >= args.warmup:
-            vals.append(r["gcups"])
+            vals.append(r["cells"] / r["seconds"] / 1e9)
+            secs.append(r["seconds"])
+            alns.append(r["pairs"] / r["seconds"])
             last = r
     value = float(np.mean(vals))
     line = {
         "impl": "reference",
-        "metric": METRIC,
+        "metric": metric_of(args.workload),
         "value": value,
         "unit": "GCUPS",
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": last["seconds"] * 1e3,
+        "ms_per_step": float(np.mean(secs)) * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "int32",
+        "dtype": "int32 (numpy int32 arrays, as align.py)",
         "data": "synthetic",
-        "alignments_per_sec": last["aln_per_s"],
-        "config": {"workload": f"{WORKLOAD}: {LENGTH}x{LENGTH} pairs, BLOSUM62, gap {GAP[0]}/{GAP[1]}",
+        "alignments_per_sec": float(np.mean(alns)),
+        "config": {"workload": WORKLOADS[args.workload]["desc"],
                    "sample_pairs_per_step": last["pairs"]},
         "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": cores, "kind": "port",
-                         "sample": f"{last['pairs']} pairs of {WORKLOAD} per step; numpy "
-                                   "restatement of align.py:79-181 in forked lanes "
-                                   "(AlignEngine use_processes=True semantics)"},
+                         "sample": f"{last['pairs']} consecutive pairs of the benched batch per "
+                                   "step; numpy restatement of align.py:79-181 over forked "
+                                   "lanes (AlignEngine use_processes=True semantics)"},
         "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# --- our arm ----------------------------------------------------------------
+def make_batch(workload: str, n: int, seed: int, alloc=None):
+    from pastis_synth import workloads
+    gen = {"config2": workloads.config2_packed, "config3": workloads.config3_packed,
+           "config5": workloads.config5_packed}[workload]
+    return gen(n, seed=seed, alloc=alloc)
 
 
 def main():
@@ -246,16 +323,16 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = len(os.sched_getaffinity(0))
-            rn = cpu_bench("numpy", args.cpu_sample)
-            rc = cpu_bench("c", max(args.cpu_sample, 8000))
+            rn = cpu_bench("numpy", args.workload, args.cpu_sample)
+            rc = cpu_bench("c", args.workload, max(args.cpu_sample, 4 * args.cpu_sample))
             cpu = {"value": rn["gcups"], "unit": "GCUPS", "cores": cores, "kind": "port",
-                   "sample": f"{rn['pairs']} {WORKLOAD} pairs; numpy restatement of "
-                             f"align.py:79-181 (the reference algorithm) over {cores} forked "
-                             f"lanes; {rn['seconds']:.1f} s wall",
+                   "sample": f"first {rn['pairs']} pairs of the benched batch (rank 0); numpy "
+                             f"restatement of align.py:79-181 (the reference algorithm) over "
+                             f"{cores} forked lanes; {rn['seconds']:.1f} s wall",
                    "alignments_per_sec": rn["aln_per_s"],
                    "c_oracle_gcups": rc["gcups"],
                    "c_oracle_note": f"plain-C restatement (oracle/sw_oracle.c), {rc['cores']} "
-                                    f"pthreads, {rc['pairs']} pairs"}
+                                    f"pthreads, first {rc['pairs']} pairs"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GCUPS", "cores": None, "kind": "port",
                    "sample": f"failed: {exc}"}
@@ -268,23 +345,31 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2303_01845_b200 import _native, blosum62, workloads
-    from paper_2303_01845_b200.batch import pack_codes
+    from paper_2303_01845_b200 import _native, blosum62
 
     lib = _native.load()
     params = _native.make_params(GAP[0], GAP[1], blosum62.MATRIX)
-    if args.workload == "config2":
-        sa, sb = workloads.config2(args.pairs, seed=2303 + rank, length=LENGTH)
-    elif args.workload == "config3":
-        sa, sb = workloads.config3_bulk(args.pairs, seed=2303 + rank)
-    else:
-        sa, sb = workloads.config5(args.pairs, seed=2303 + rank)
-    arena_np, table_np = pack_codes(sa, sb)
+
+    def pinned(nbytes):
+        ptr = lib.sw_host_alloc(nbytes)
+        if not ptr:
+            raise RuntimeError("sw_host_alloc failed")
+        return ptr, np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(ptr))
+
+    pins = []
+
+    def alloc(nbytes):
+        ptr, arr = pinned(nbytes)
+        pins.append(ptr)
+        return arr
+
+    # this rank's batch, generated straight into pinned host memory
+    arena_np, table_np = make_batch(args.workload, args.pairs, 2303 + rank, alloc=alloc)
     cells = int(np.dot(table_np["a_len"].astype(np.int64), table_np["b_len"].astype(np.int64)))
     n_pairs = len(table_np)
 
     # device-resident inputs for `value`
-    d_arena = torch.from_numpy(arena_np.copy()).to(dev)
+    d_arena = torch.from_numpy(arena_np).to(dev)
     d_pairs = torch.from_numpy(table_np.view(np.uint8).copy()).to(dev)
     d_out = torch.empty(n_pairs * 32, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -306,11 +391,11 @@ def main():
                                     n_pairs, params, d_out.data_ptr(), device=local,
                                     stream=stream.cuda_stream)
 
-    step_ms, fwd_ms, rev_ms, tb_ms, launches = [], [], [], [], 0
-    tm = None
+    step_ms, launches = [], 0
+    tms = []
     with ClockSampler(local) as clocks:
-        # warm-up also lets the first nvidia-smi query (which stalls the
-        # driver briefly) happen before the timed region
+        # warm-up also lets the first clock query (which stalls the driver
+        # briefly) happen before the timed region
         for _ in range(args.warmup):
             device_step()
         t_wait = time.time()
@@ -329,35 +414,26 @@ def main():
                 e1.record(stream)
                 torch.cuda.synchronize()
                 step_ms.append(e0.elapsed_time(e1))
-                fwd_ms.append(tm["forward_ms"])
-                rev_ms.append(tm["reverse_ms"])
-                tb_ms.append(tm["traceback_ms"])
+                tms.append(tm)
                 launches += tm["launches"]
         barrier()
     dev_ms = max_over_ranks(float(np.sum(step_ms)))
-    fwd_total = max_over_ranks(float(np.sum(fwd_ms)))
     total_cells = cells * world * args.steps
     value = total_cells / (dev_ms / 1e3) / 1e9
+    rec_dev = d_out.cpu().numpy().view(_native.RESULT_DTYPE)
 
     # end to end through the host C-ABI call with pinned buffers
-    def pinned(nbytes):
-        ptr = lib.sw_host_alloc(nbytes)
-        if not ptr:
-            raise RuntimeError("sw_host_alloc failed")
-        return ptr, np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(ptr))
-
-    pa_ptr, pa = pinned(max(1, arena_np.size))
-    pa[: arena_np.size] = arena_np
-    pp_ptr, pp = pinned(table_np.nbytes)
-    pp[:] = table_np.view(np.uint8)
     po_ptr, po = pinned(n_pairs * 32)
-    host_arena = pa[: arena_np.size]
+    pins.append(po_ptr)
+    pp_ptr, pp = pinned(table_np.nbytes)
+    pins.append(pp_ptr)
+    pp[:] = table_np.view(np.uint8)
     host_pairs = pp.view(_native.PAIR_DTYPE)
     host_out = po.view(_native.RESULT_DTYPE)
 
     def host_step():
         t0 = time.perf_counter()
-        _, t = _native.align_host(host_arena, host_pairs, params, device=local, out=host_out)
+        _, t = _native.align_host(arena_np, host_pairs, params, device=local, out=host_out)
         return (time.perf_counter() - t0) * 1e3, t
 
     for _ in range(max(1, args.warmup)):
@@ -367,32 +443,45 @@ def main():
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
-        ms, tmh = host_step()
+        ms, _ = host_step()
         e2e_ms.append(ms)
     barrier()
     e2e_total = max_over_ranks(float(np.sum(e2e_ms)))
     e2e_value = total_cells / (e2e_total / 1e3) / 1e9
-    ok = bool((host_out["status"] == 0).all())
+    ok = bool((host_out["status"] == 0).all()) and bool((host_out == rec_dev).all())
+
+    # end to end through the reference-shaped Python API
+    api = None
+    if not args.no_api and world == 1:
+        api = api_leg(args, arena_np, table_np, cells, flush, torch)
 
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
+        for p in pins:
+            lib.sw_host_free(p)
         return
 
-    # integer/DPX roofline of the forward kernel (K1), measured DPX issue rate
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     csum = clocks.summary()
     # Integer issue roofline of the minimal Gotoh cell in packed u16x2 form
-    # (two cells per lane-op): 4 adds + 5 maxes = 9 issue slots per word, and
-    # no formulation needs fewer pipe cycles (measured on B200: VIMNMX full
-    # rate on the ALU pipe, IMAD half rate on the FMA pipe, DPX fused ops half
-    # rate on the ALU pipe -> profiles/r01/{dpx_rate,pipe_mix,mix2}.txt).
+    # (two cells per lane-op): 4 adds + 5 maxes = 9 issue slots per word
+    # (measured on B200: VIMNMX full rate on the ALU pipe, IMAD half rate on
+    # the FMA pipe, fused DPX ops half rate on the ALU pipe ->
+    # profiles/r01/{dpx_rate,pipe_mix,mix2}.txt).
     slots_per_word = 9.0
     clk_ghz = (csum.get("sm_max_mhz") or 1965.0) / 1e3
     peak_gcups = sms * clk_ghz * 4 * 32 * 2 / slots_per_word
-    fwd_gcups = cells * args.steps / (float(np.sum(fwd_ms)) / 1e3) / 1e9
+    mean = lambda key: float(np.mean([t[key] for t in tms]))  # noqa: E731
+    fwd_ms = mean("forward_ms")
+    fwd_gcups = cells / (fwd_ms / 1e3) / 1e9
+    dominant = ("k_score_cta_packed<8> (K1cp: forward, 2 long pairs per CTA)"
+                if args.workload == "config5" else
+                "k_score_packed<R> (K1p: forward, 2 pairs per warp, R = 4..16 rows/lane "
+                "classes running concurrently)")
+    cc = computed_cells(table_np)
     line = {
-        "metric": METRIC,
+        "metric": metric_of(args.workload),
         "value": value,
         "unit": "GCUPS",
         "n_gpus": world,
@@ -402,53 +491,92 @@ def main():
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "int32",
+        "dtype": DTYPE,
         "data": "synthetic",
         "alignments_per_sec": n_pairs * world * args.steps / (dev_ms / 1e3),
         "forward_gcups": fwd_gcups,
-        "phase_ms_per_step": {"forward": float(np.mean(fwd_ms)), "reverse": float(np.mean(rev_ms)),
-                              "traceback": float(np.mean(tb_ms))},
+        "phase_ms_per_step": {
+            "forward": fwd_ms,
+            "tile_traceback_k5": mean("tile_tb_ms"),
+            "traceback_past_forward": mean("fwd_tail_ms"),
+            "reverse": mean("reverse_ms"),
+            "box_traceback": mean("traceback_ms"),
+            "note": "forward = fork -> last forward kernel (K1p classes + long-pair K1cp/K1, "
+                    "concurrent streams); tile_traceback_k5 = union of K5's class-stream "
+                    "intervals (overlaps other classes' forward); traceback_past_forward = "
+                    "how long K5 runs after the forward phase; reverse/box_traceback = the "
+                    "long-pair chain",
+        },
         "results_ok": ok,
-        "config": {"workload": (f"{WORKLOAD}: {args.pairs} pairs/GPU of {LENGTH}x{LENGTH}, "
-                                f"BLOSUM62, gap {GAP[0]}/{GAP[1]}, 50% homologs")
-                   if args.workload == "config2" else
-                   f"{args.workload}: {args.pairs} pairs/GPU, BLOSUM62, gap {GAP[0]}/{GAP[1]}",
-                   "pairs_per_gpu": args.pairs, "cells_per_gpu_per_step": cells,
+        "config": {"workload": WORKLOADS[args.workload]["desc"],
+                   "pairs_per_gpu": n_pairs, "cells_per_gpu_per_step": cells,
                    "l2": "flushed between timed steps (256 MiB memset, outside the events)",
-                   "parallelism": f"weak-scaled shards x{world}"},
-        "roofline": {"bound": "int-issue", "kernel": "k_score_packed<R=10> (K1 forward, 2 pairs/warp)",
+                   "parallelism": f"one process per GPU x{world}, weak scaling"},
+        "roofline": {"bound": "int-issue", "kernel": dominant,
                      "achieved": fwd_gcups, "peak": peak_gcups, "unit": "GCUPS",
                      "frac": fwd_gcups / peak_gcups,
+                     "achieved_basis": "algorithmic cells (sum |a||b|) / forward-phase time "
+                                       "(CUDA events on the class streams)",
                      "peak_basis": f"{sms} SMs x {clk_ghz:.3f} GHz x 4 SMSP x 32 lanes x 2 cells "
                                    f"(u16x2) / {slots_per_word:.0f} issue slots per packed Gotoh "
                                    "cell (4 adds + 5 maxes); pipe rates measured in tools/microbench",
-                     "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 32/(m*n) = 0.0070 B "
-                                 "-> non-binding (HBM would allow ~9e14 CUPS)",
-                     # context for `frac`: the ALU-pipe ceiling of the cell as written
-                     # (PRMT 2 + 3 VIADDMNMX 6 + VIMNMX3 2 + VIMNMX 1 = 11 ALU-pipe
-                     # cycles per packed row-word; ncu shows that pipe at 74 %), and the
-                     # cells the kernel computes per algorithmic cell (strip padding
-                     # 320/300 rows x wavefront skew (n+31)/n steps at config 2)
+                     "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 56/(m*n) "
+                                 f"= {(arena_np.size + 56 * n_pairs) / cells:.4f} B -> non-binding",
                      "alu_pipe_ceiling": sms * clk_ghz * 4 * 64 / 11.0,
-                     "computed_cells_per_cell": (320 * 331) / (300 * 300)
-                     if args.workload == "config2" else None,
-                     **traffic_fields(fwd_ms, args)},
+                     **cc,
+                     **ncu_fields(args.workload, dev_ms / args.steps)},
         "e2e": {"value": e2e_value, "unit": "GCUPS",
                 "h2d_bytes_per_step": int(arena_np.size + table_np.nbytes),
                 "d2h_bytes_per_step": int(n_pairs * 32),
                 "ms_per_step": e2e_total / args.steps,
-                "alignments_per_sec": n_pairs * world * args.steps / (e2e_total / 1e3)},
+                "alignments_per_sec": n_pairs * world * args.steps / (e2e_total / 1e3),
+                "entry": "sw_align_batch (C ABI, pinned host buffers)"},
         "gpu_launches": int(launches),
         "clocks": csum,
     }
+    if api is not None:
+        line["api_e2e"] = api
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
-    lib.sw_host_free(pa_ptr)
-    lib.sw_host_free(pp_ptr)
-    lib.sw_host_free(po_ptr)
+    for p in pins:
+        lib.sw_host_free(p)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def api_leg(args, arena_np, table_np, cells, flush, torch) -> dict:
+    """AlignEngine(...).submit([(str, str, None), ...]).result() -- the
+    reference's batch seam (align.py:299-347) -- on the same batch."""
+    import paper_2303_01845_b200 as sw
+    raw = arena_np.tobytes()
+    pairs = [(raw[a:a + la].decode(), raw[b:b + lb].decode(), None)
+             for a, b, la, lb in table_np.tolist()]
+    del raw
+    params = sw.AlignParams(gap_open=GAP[0], gap_extend=GAP[1])
+    eng = sw.AlignEngine(params, lanes=1, use_processes=True)
+    eng.start()
+    walls, phases = [], []
+    steps = min(args.steps, 3)          # host-heavy leg: a few steps suffice
+    for step in range(1 + steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        results, errors, counters, lanes = eng.submit(pairs).result()
+        dt = time.perf_counter() - t0
+        if step >= 1:
+            walls.append(dt)
+            phases.append(getattr(eng, "last_phases", {}))
+    eng.close()
+    assert not errors and len(results) == len(pairs)
+    wall = float(np.mean(walls))
+    out = {"value": cells / wall / 1e9, "unit": "GCUPS", "ms_per_step": wall * 1e3,
+           "alignments_per_sec": len(pairs) / wall,
+           "entry": "AlignEngine(lanes=1, use_processes=True).submit(list[(str, str, None)])"
+                    ".result()"}
+    if phases and phases[0]:
+        out["phase_ms"] = {k: float(np.mean([p[k] for p in phases])) * 1e3 for k in phases[0]}
+    return out
 
 
 if __name__ == "__main__":

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SW_ABI_VERSION 1
+#define SW_ABI_VERSION 2
 
 /* call-level return codes */
 #define SW_OK 0
@@ -97,6 +97,10 @@ typedef struct sw_timing_t { /* filled when non-NULL; device times from CUDA eve
   uint64_t rev_cells;      /* cells scored by K2 */
   double host_plan_ms;     /* host time until the length plan is known (one small sync) */
   double host_setup_ms;    /* host time spent sizing / allocating cached device buffers */
+  double tile_tb_ms;       /* K5 tile traceback: union of its per-class stream intervals
+                              (they overlap the forward pass of the other classes) */
+  double fwd_tail_ms;      /* forward phase end -> last K5 done (traceback not hidden
+                              behind the forward pass) */
 } sw_timing_t;
 
 /* Number of visible CUDA devices (0 when none). */

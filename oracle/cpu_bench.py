@@ -41,12 +41,20 @@ def _run_chunk(bounds):
     return out
 
 
-def sample_pairs(workload: str, n: int, seed: int):
-    from paper_2303_01845_b200 import workloads
-    gen = {"config2": workloads.config2, "config3": workloads.config3,
-           "config5": workloads.config5}[workload]
-    sa, sb = gen(n, seed=seed)
-    return [(a.decode(), b.decode()) for a, b in zip(sa, sb)]
+def sample_pairs(workload: str, n: int, seed: int, offset: int = 0):
+    """Pairs [offset, offset + n) of the batch bench.py times for `workload`
+    (pastis_synth's packed generators: the first k pairs of a batch do not
+    depend on its size), as (str, str)."""
+    from pastis_synth import workloads
+    gen = {"config2": workloads.config2_packed, "config3": workloads.config3_packed,
+           "config5": workloads.config5_packed}[workload]
+    arena, table = gen(offset + n, seed=seed)
+    raw = arena.tobytes()
+    out = []
+    for p in table[offset:offset + n].tolist():
+        a_off, b_off, la, lb = p
+        out.append((raw[a_off:a_off + la].decode(), raw[b_off:b_off + lb].decode()))
+    return out
 
 
 def time_numpy(pairs, gap, mat, procs: int) -> dict:
@@ -83,6 +91,7 @@ def main():
     ap.add_argument("--workload", default="config2")
     ap.add_argument("--pairs", type=int, default=2000)
     ap.add_argument("--seed", type=int, default=2303)
+    ap.add_argument("--offset", type=int, default=0)
     ap.add_argument("--procs", type=int, default=0)
     ap.add_argument("--gap-open", type=int, default=11)
     ap.add_argument("--gap-extend", type=int, default=1)
@@ -90,7 +99,7 @@ def main():
     procs = args.procs or len(os.sched_getaffinity(0))
     from paper_2303_01845_b200 import blosum62
     mat = np.asarray(blosum62.MATRIX, dtype=np.int32)
-    pairs = sample_pairs(args.workload, args.pairs, args.seed)
+    pairs = sample_pairs(args.workload, args.pairs, args.seed, args.offset)
     gap = (args.gap_open, args.gap_extend)
     if args.mode == "numpy":
         r = time_numpy(pairs, gap, mat, procs)

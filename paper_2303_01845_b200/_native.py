@@ -83,6 +83,8 @@ class SwTiming(ctypes.Structure):
         ("rev_cells", ctypes.c_uint64),
         ("host_plan_ms", ctypes.c_double),
         ("host_setup_ms", ctypes.c_double),
+        ("tile_tb_ms", ctypes.c_double),
+        ("fwd_tail_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -46,7 +46,17 @@ def build_oracle(force: bool = False) -> str:
     return target
 
 
+def build_synth(force: bool = False) -> str:
+    """The bench/test workload generator (pastis_synth/gen.c, gcc)."""
+    sdir = os.path.join(ROOT, "pastis_synth")
+    target = os.path.join(sdir, "libsynth.so")
+    if force or _stale(target, [os.path.join(sdir, "gen.c")]):
+        subprocess.run(["make", "-B" if force else "-s", "-C", sdir, "libsynth.so"], check=True)
+    return target
+
+
 if __name__ == "__main__":
     force = "--force" in sys.argv
     print(build_native(force=force, verbose="-v" in sys.argv))
     print(build_oracle(force=force))
+    print(build_synth(force=force))

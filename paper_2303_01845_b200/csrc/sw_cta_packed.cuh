@@ -331,7 +331,11 @@ k_jend(KArgs A, int stage, int cls) {
         A.out[k] = r;
       } else {
         const uint64_t area = (uint64_t)(i_end + 1) * (uint64_t)(j_end + 1);
-        if ((uint64_t)best * best * 8ull > 49ull * area) {   // homolog: box = prefix
+        // homolog: box = prefix.  So is a pair whose score does not fit the
+        // reverse pass's scaled int32 domain (best >= kScaledLimit: only the
+        // u16x2 forward reaches it without the wide re-run); the box fill is
+        // plain int32.
+        if ((uint64_t)best * best * 8ull > 49ull * area || best >= kScaledLimit) {
           st->i0 = 0;
           st->j0 = 0;
           list_push(A, 2, class_of(i_end + 1), (uint32_t)k);

@@ -330,7 +330,10 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
 
   KArgs A;
   memset(&A, 0, sizeof(A));
-  A.codes = (const uint8_t *)c->codes.p;
+  // codes[i] = lut[raw[i]] at the raw arena's address modulo 16, so k_encode
+  // moves aligned 128-bit words whatever the caller's pointer alignment
+  uint8_t *codes = (uint8_t *)c->codes.p + ((uintptr_t)d_arena & 15u);
+  A.codes = codes;
   A.raw = d_arena;
   A.pairs = d_pairs;
   A.st = (PairState *)c->st.p;
@@ -370,7 +373,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   if (!arena_done) {   // resident arena: encode first, every kernel reads codes
     const int threads = 256;
     uint64_t blocks = std::min<uint64_t>((arena_bytes / 16 + threads) / threads + 1, (uint64_t)c->sms * 8);
-    k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, (uint8_t *)c->codes.p, arena_bytes,
+    k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, codes, arena_bytes,
                                                  (const uint8_t *)c->lut.p);
     ++launches;
   }
@@ -444,7 +447,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   CU(cudaEventRecord(c->ev[1], s));
 
   uint32_t h_cnt[kStages * kNumClasses];
-  double fwd_ms = 0.0, rev_ms = 0.0, tb_ms = 0.0;
+  double fwd_ms = 0.0, rev_ms = 0.0, tb_ms = 0.0, tile_ms = 0.0, tail_ms = 0.0;
   uint64_t wide = 0;
   for (int pround = 0;; ++pround) {
     CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
@@ -471,7 +474,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
       CU(cudaStreamWaitEvent(s, arena_done, 0));
       const int threads = 256;
       uint64_t blocks = std::min<uint64_t>((arena_bytes / 16 + threads) / threads + 1, (uint64_t)c->sms * 8);
-      k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, (uint8_t *)c->codes.p, arena_bytes,
+      k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, codes, arena_bytes,
                                                    (const uint8_t *)c->lut.p);
       ++launches;
     }
@@ -564,6 +567,26 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     double f = ev_ms(c->ev_fork, c->ev[7]);
     for (int cls = 0; cls < kNumClasses; ++cls) f = std::max(f, (double)ev_ms(c->ev_fork, c->ev_k1[cls]));
     fwd_ms += f;
+    {
+      // K5 runs on the class streams right after each class's forward: the
+      // union of its [ev_k1, ev_tb] intervals, and how far it runs past the
+      // forward phase
+      std::pair<double, double> iv[kNumClasses];
+      double tb_end = 0.0;
+      for (int cls = 0; cls < kNumClasses; ++cls) {
+        iv[cls] = {ev_ms(c->ev_fork, c->ev_k1[cls]), ev_ms(c->ev_fork, c->ev_tb[cls])};
+        tb_end = std::max(tb_end, iv[cls].second);
+      }
+      std::sort(iv, iv + kNumClasses);
+      double cur0 = iv[0].first, cur1 = iv[0].first, uni = 0.0;
+      for (auto &x : iv) {
+        if (x.first > cur1) { uni += cur1 - cur0; cur0 = x.first; cur1 = x.first; }
+        cur1 = std::max(cur1, x.second);
+      }
+      uni += cur1 - cur0;
+      tile_ms += uni;
+      tail_ms += std::max(0.0, tb_end - f);
+    }
     rev_ms += ev_ms(c->ev[2], c->ev[3]);
     wide += h_cnt[3 * kNumClasses];
     uint32_t deferred = 0;
@@ -589,6 +612,8 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     tm->wide_pairs += wide;
     tm->host_plan_ms += h1 - h0;
     tm->host_setup_ms += h2 - h1;
+    tm->tile_tb_ms += tile_ms;
+    tm->fwd_tail_ms += tail_ms;
   }
   if (s != user_s) {
     CU(cudaEventRecord(c->ev_out, s));

@@ -1243,11 +1243,21 @@ __global__ void k_walk(KArgs A, const uint32_t *only, uint32_t n_only) {
 }
 
 // Byte -> residue code (align.py:27-30: unknown bytes score as 'X').
+// `raw` may sit at any byte address (a caller's device buffer or a slice of
+// one); `codes` must have the same address modulo 16 (the caller offsets it),
+// so the body moves as aligned 128-bit words and only the unaligned head and
+// tail go byte by byte.
 __global__ void k_encode(const uint8_t *__restrict__ raw, uint8_t *__restrict__ codes, uint64_t n,
                          const uint8_t *__restrict__ lut) {
   __shared__ uint8_t slut[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) slut[i] = lut[i];
   __syncthreads();
+  uint64_t head = (16u - ((uintptr_t)raw & 15u)) & 15u;
+  if (head > n) head = n;
+  if (blockIdx.x == 0 && threadIdx.x < head) codes[threadIdx.x] = slut[raw[threadIdx.x]];
+  raw += head;
+  codes += head;
+  n -= head;
   const uint64_t n16 = n / 16;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
        i += (uint64_t)gridDim.x * blockDim.x) {

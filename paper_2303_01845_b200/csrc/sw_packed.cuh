@@ -34,6 +34,7 @@ constexpr int kProfUnroll = K1P_PROF_UNROLL;   // code groups per profile-build 
 constexpr int kStageBytesP = 17 * 8 * 8;         // (16 boundaries + dummy) x 8 steps x (Ho2, F2)
 constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs
 constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
+constexpr int32_t kTileMax = 32767;               // largest score k_tb's int16 tiles hold
 // Profile table of the packed kernels: matT[a][code] = s(code, a) + open as
 // u8 (a = row residue, code = column residue; PAD row/column -> 0), rows
 // padded to 32 bytes so four codes load as one word.  kMatTBytes replaces
@@ -453,7 +454,12 @@ k_score_packed(KArgs A, int stage, int cls) {
         const int32_t i_end = 0xFFFF - (int32_t)((key >> 16) & 0xFFFF);
         st->i0 = 0;
         st->j0 = 0;
-        if (overflow) {                        // both halves suspect: wide path
+        // The tile traceback (k_tb) replays H/E/F in int16 shared-memory
+        // tiles: exact while best <= 32767 (every replayed value lies in
+        // [-open, best]).  A pair scoring above that (only reachable with
+        // large custom matrices: BLOSUM62 tops out at 11 per residue) takes
+        // the int32 path: wide forward, reverse pass, box traceback.
+        if (overflow || best > kTileMax) {     // overflow: both halves suspect
           st->flags = kFlagWide;
           list_push(A, 3, 0, (uint32_t)P[h].k);
         } else if (best == 0) {

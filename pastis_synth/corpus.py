@@ -16,7 +16,7 @@ seqio.write_fasta (seqio.py:95-98).
 
 import random
 
-from .seqio import SequenceRecord
+from paper_2303_01845_b200.seqio import SequenceRecord
 
 STANDARD_RESIDUES = "ARNDCQEGHILKMFPSTWYV"
 

@@ -175,3 +175,86 @@ def _config3_chunk(n: int, seed: int):
     for k, s in zip(r_idx.tolist(), b_r):
         seqs_b[k] = s
     return _split(a, la), seqs_b
+
+
+# ---------------------------------------------------------------------------
+# Packed generators (gen.c): the same models, written straight into a byte
+# arena + sw_pair_t table by multi-threaded C -- ~50x faster than the numpy
+# generators above (different random streams; the tests check the GPU against
+# the CPU oracle on whatever these produce, and the bench's full-size parity
+# test uses exactly the batch the bench times).
+# ---------------------------------------------------------------------------
+import ctypes as _ct
+import os as _os
+
+_HERE = _os.path.dirname(_os.path.abspath(__file__))
+_LIB = None
+PAIR_DTYPE = np.dtype([("a_off", "<u8"), ("b_off", "<u8"), ("a_len", "<u4"), ("b_len", "<u4")])
+
+
+class _Cfg(_ct.Structure):
+    _fields_ = [("kind", _ct.c_int), ("seed", _ct.c_uint64), ("length", _ct.c_uint32),
+                ("lo", _ct.c_uint32), ("hi", _ct.c_uint32), ("hom_frac", _ct.c_double),
+                ("sub_rate", _ct.c_double), ("indel_rate", _ct.c_double)]
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        path = _os.path.join(_HERE, "libsynth.so")
+        if not _os.path.exists(path) or (_os.path.getmtime(path) <
+                                         _os.path.getmtime(_os.path.join(_HERE, "gen.c"))):
+            import subprocess
+            subprocess.run(["make", "-s", "-B", "-C", _HERE, "libsynth.so"], check=True)
+        lib = _ct.CDLL(path)
+        vp, u64 = _ct.c_void_p, _ct.c_uint64
+        lib.syn_lengths.argtypes = [_ct.POINTER(_Cfg), u64, vp, vp, vp]
+        lib.syn_lengths.restype = _ct.c_int
+        lib.syn_fill.argtypes = [_ct.POINTER(_Cfg), u64, vp, vp, vp, _ct.c_int]
+        lib.syn_fill.restype = _ct.c_int
+        _LIB = lib
+    return _LIB
+
+
+def packed(kind: int, n: int, seed: int, *, length: int = 300, lo: int = 2000, hi: int = 35000,
+           hom_frac: float = 0.5, sub_rate: float = 0.30, indel_rate: float = 0.08,
+           alloc=None, threads: int = 0):
+    """(arena uint8, table PAIR_DTYPE) of `n` pairs of config `kind` (2, 3, 5);
+    pair k's a and b sit back to back in the arena.  `alloc(nbytes)` may
+    supply the arena buffer (e.g. pinned host memory)."""
+    lib = _lib()
+    c = _Cfg(kind, seed, length, lo, hi, hom_frac, sub_rate, indel_rate)
+    la = np.empty(n, np.uint32)
+    lb = np.empty(n, np.uint32)
+    hom = np.empty(n, np.uint8)
+    if lib.syn_lengths(_ct.byref(c), n, la.ctypes.data, lb.ctypes.data, hom.ctypes.data):
+        raise ValueError(f"unknown workload kind {kind}")
+    tot = la.astype(np.uint64) + lb
+    ends = np.cumsum(tot, dtype=np.uint64)
+    table = np.empty(n, PAIR_DTYPE)
+    table["a_off"] = ends - tot
+    table["b_off"] = table["a_off"] + la
+    table["a_len"] = la
+    table["b_len"] = lb
+    nbytes = int(ends[-1]) if n else 0
+    arena = alloc(max(nbytes, 1)) if alloc is not None else np.empty(max(nbytes, 1), np.uint8)
+    lib.syn_fill(_ct.byref(c), n, table.ctypes.data, hom.ctypes.data, arena.ctypes.data,
+                 threads or len(_os.sched_getaffinity(0)))
+    return arena[: max(nbytes, 1)], table
+
+
+def config2_packed(n: int, seed: int = 2303, length: int = 300, **kw):
+    """Config 2: n pairs of length x length, half homologs."""
+    return packed(2, n, seed, length=length, **kw)
+
+
+def config3_packed(n: int, seed: int = 2303, **kw):
+    """Config 3: 1M-pair-scale skewed lengths 30-2000 (lognormal), half homologs."""
+    return packed(3, n, seed, **kw)
+
+
+def config5_packed(n: int, seed: int = 2303, lo: int = 2000, hi: int = 35000, hom_frac: float = 0.0,
+                   **kw):
+    """Config 5: lengths U[lo, hi]; hom_frac of the b's homologs of their a
+    (0 = the BASELINE config: independent pairs)."""
+    return packed(5, n, seed, lo=lo, hi=hi, hom_frac=hom_frac, **kw)

@@ -34,7 +34,7 @@ from pastislite import seqio as ref_seqio  # noqa: E402
 from pastislite import synth as ref_synth  # noqa: E402
 from pastislite.alphabet import ALPHABET, INDEX  # noqa: E402
 
-from paper_2303_01845_b200 import workloads  # noqa: E402
+from pastis_synth import workloads  # noqa: E402
 
 STD = "ARNDCQEGHILKMFPSTWYV"
 FIELDS = ("score", "i_begin", "i_end", "j_begin", "j_end", "matches", "aln_len", "cells")

@@ -27,7 +27,7 @@ def test_library_exports_every_symbol():
     lib = _native.load()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.sw_abi_version() == 1
+    assert lib.sw_abi_version() == 2
 
 
 def test_library_built_for_sm100a():

@@ -25,7 +25,8 @@ def _worker(rank, world, port, q):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     from oracle import oracle
-    from paper_2303_01845_b200 import blosum62, workloads
+    from paper_2303_01845_b200 import blosum62
+    from pastis_synth import workloads
     from paper_2303_01845_b200._native import RESULT_DTYPE
     from paper_2303_01845_b200.batch import pack_codes
     from paper_2303_01845_b200.distributed import align_distributed

@@ -15,7 +15,8 @@ from oracle import oracle
 pytestmark = pytest.mark.gpu
 
 import paper_2303_01845_b200 as sw  # noqa: E402
-from paper_2303_01845_b200 import _native, workloads  # noqa: E402
+from paper_2303_01845_b200 import _native  # noqa: E402
+from pastis_synth import workloads  # noqa: E402
 from paper_2303_01845_b200.batch import pack_codes, pack_pairs  # noqa: E402
 
 
@@ -224,25 +225,6 @@ def test_symmetric_score_property():
     assert (rec_s["score"] == rec["score"]).all()
 
 
-def test_full_config2_properties():
-    """Config 2 at full size: size-independent checks + an oracle sample."""
-    sa, sb = workloads.config2(100_000, seed=2303)
-    arena, table = pack_codes(sa, sb)
-    p = _native.make_params(11, 1, matrix("blosum62"))
-    rec, tm = _native.align_host(arena, table, p)
-    assert (rec["status"] == 0).all()
-    pos = rec["score"] > 0
-    assert ((rec["i_begin"] <= rec["i_end"]) | ~pos).all()
-    assert ((rec["matches"] <= rec["aln_len"]) | ~pos).all()
-    span = np.maximum(rec["i_end"] - rec["i_begin"], rec["j_end"] - rec["j_begin"]) + 1
-    assert ((rec["aln_len"] >= span) | ~pos).all()
-    assert tm["cells"] == 100_000 * 300 * 300
-    pick = np.random.default_rng(1).choice(len(table), 400, replace=False)
-    ref = oracle.align_batch_c(arena, table[pick], 11, 1, matrix("blosum62"), threads=16)
-    got = np.stack([rec[f][pick] for f in FIELDS], axis=1)
-    assert (got == ref[:, :7]).all()
-
-
 def test_cta_per_pair_long_vs_oracle():
     """Pairs of >= 4 strips (2048+ rows) take the CTA-per-pair forward and
     reverse kernels: exact against the full C oracle."""
@@ -262,40 +244,6 @@ def test_cta_per_pair_long_vs_oracle():
         _oracle_compare(sa, sb, go, ge)
 
 
-def test_config5_scale_properties():
-    """A config-5-size pair (20k x 25k): score and end cell against the O(n)
-    score oracle, begin/matches/length via the box lemma (re-aligning the
-    reported spans must reproduce them)."""
-    sa, sb = workloads.config5(2, seed=55, lo=20000, hi=25000)
-    arena, table = pack_codes(sa, sb)
-    mat = matrix("blosum62")
-    rec, _ = _native.align_host(arena, table, _native.make_params(11, 1, mat))
-    for k in range(len(table)):
-        a, b = sa[k], sb[k]
-        best, i_end, j_end = oracle.score_c(a, b, 11, 1, mat)
-        r = rec[k]
-        assert (int(r["score"]), int(r["i_end"]), int(r["j_end"])) == (best, i_end, j_end)
-        sub = oracle.align_c(a[r["i_begin"]:i_end + 1], b[r["j_begin"]:j_end + 1], 11, 1, mat)
-        assert sub[0] == best and sub[1] == 0 and sub[3] == 0
-        assert (sub[5], sub[6]) == (int(r["matches"]), int(r["aln_len"]))
-
-
-def test_full_config3_properties():
-    sa, sb = workloads.config3(200_000, seed=2304)
-    arena, table = pack_codes(sa, sb)
-    p = _native.make_params(11, 1, matrix("blosum62"))
-    rec, tm = _native.align_host(arena, table, p)
-    assert (rec["status"] == 0).all()
-    pos = rec["score"] > 0
-    assert ((rec["i_end"] < table["a_len"].astype(np.int64)) | ~pos).all()
-    assert ((rec["j_end"] < table["b_len"].astype(np.int64)) | ~pos).all()
-    assert ((rec["matches"] <= rec["aln_len"]) | ~pos).all()
-    pick = np.random.default_rng(2).choice(len(table), 300, replace=False)
-    ref = oracle.align_batch_c(arena, table[pick], 11, 1, matrix("blosum62"), threads=16)
-    got = np.stack([rec[f][pick] for f in FIELDS], axis=1)
-    assert (got == ref[:, :7]).all()
-
-
 @pytest.mark.parametrize("pool_mb,n_pairs", [(16, 3000), (4, 1000)])
 def test_pool_overflow_falls_back_exactly(pool_mb, n_pairs):
     """With a small traceback pool the packed pass defers pairs to further
@@ -309,7 +257,8 @@ def test_pool_overflow_falls_back_exactly(pool_mb, n_pairs):
     code = r'''
 import json, sys, numpy as np
 sys.path.insert(0, ".")
-from paper_2303_01845_b200 import _native, workloads, blosum62
+from paper_2303_01845_b200 import _native, blosum62
+from pastis_synth import workloads
 from paper_2303_01845_b200.batch import pack_codes
 from oracle import oracle
 sa, sb = workloads.config3(int(sys.argv[1]), seed=8)
@@ -377,7 +326,8 @@ import json, sys, numpy as np
 sys.path.insert(0, ".")
 sys.path.insert(0, "tests")
 from conftest import FIELDS, expect_tuple, load_golden, matrix
-from paper_2303_01845_b200 import _native, workloads
+from paper_2303_01845_b200 import _native
+from pastis_synth import workloads
 from paper_2303_01845_b200.batch import pack_codes, pack_pairs
 from oracle import oracle
 bad = 0

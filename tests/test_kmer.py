@@ -9,7 +9,8 @@ import pytest
 
 from conftest import load_golden
 from oracle import kmer_oracle
-from paper_2303_01845_b200 import _native, corpus
+from paper_2303_01845_b200 import _native
+from pastis_synth import corpus
 
 GOLD = load_golden("kmer_candidates.json")["cases"]
 

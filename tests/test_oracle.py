@@ -58,3 +58,25 @@ def test_batch_oracle_threads():
 def test_empty_rejected():
     with pytest.raises(ValueError):
         oracle.align_c("", "A", 11, 1, matrix("blosum62"))
+
+
+def test_long_pair_oracle_matches_full_oracle():
+    """orc_align_long (O(sqrt(m) n) memory, used for config-5-size pairs) equals
+    orc_align on homologs and unrelated pairs across gap settings, including
+    traceback walks that cross its checkpoint blocks."""
+    from pastis_synth import workloads
+    mat = matrix("blosum62")
+    for kind, kw in ((3, {}), (5, dict(lo=200, hi=1500, hom_frac=0.7)), (2, dict(length=120))):
+        arena, table = workloads.packed(kind, 120, 11, **kw)
+        for go, ge in ((11, 1), (11, 2), (5, 5), (3, 0), (0, 0)):
+            full = oracle.align_batch_c(arena, table, go, ge, mat, threads=8)
+            lng = oracle.align_batch_c(arena, table, go, ge, mat, threads=8, long=True)
+            assert (full == lng).all(), (kind, go, ge)
+
+
+def test_packed_generator_is_deterministic():
+    from pastis_synth import workloads
+    a1, t1 = workloads.config3_packed(5000, seed=3, threads=1)
+    a2, t2 = workloads.config3_packed(5000, seed=3, threads=6)
+    assert (a1 == a2).all() and (t1 == t2).all()
+    assert t1["a_len"].min() >= 30 and t1["a_len"].max() <= 2000

@@ -14,7 +14,8 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2303_01845_b200 import corpus, pipeline  # noqa: E402
+from paper_2303_01845_b200 import pipeline  # noqa: E402
+from pastis_synth import corpus  # noqa: E402
 
 REF_DIGEST = {(100_000, 4): "a841c454a5f50663d63d91985af2dda1ae888eb0d1bea62d09531f86d5a3f45a",
               (1000, 0): "e08ae282e079121bf115d332ba6dd79838dd2b4811c8fefd2ce39c66cbdfe655"}

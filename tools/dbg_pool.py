@@ -2,7 +2,8 @@
 import json, sys, os
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2303_01845_b200 import _native, workloads, blosum62
+from paper_2303_01845_b200 import _native, blosum62
+from pastis_synth import workloads
 from paper_2303_01845_b200.batch import pack_codes
 from oracle import oracle
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 3000

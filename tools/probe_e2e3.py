@@ -2,7 +2,8 @@
 import ctypes, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-from paper_2303_01845_b200 import _native, blosum62, workloads
+from paper_2303_01845_b200 import _native, blosum62
+from pastis_synth import workloads
 from paper_2303_01845_b200.batch import pack_codes
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000000
 sa, sb = workloads.config3_bulk(n)
