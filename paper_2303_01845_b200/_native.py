@@ -279,3 +279,78 @@ def kmer_candidates(arena: np.ndarray, offsets: np.ndarray, lengths: np.ndarray,
         _check(rc)
         d = {name: getattr(st, name) for name, _ in SwKmerStats._fields_ if name != "pad"}
         return out[: st.performed], d
+
+
+class PinnedPool:
+    """Recycled pinned (page-locked, cudaHostAllocPortable) host buffers.
+
+    cudaHostAlloc costs far more than the copies it speeds up, so buffers are
+    kept and reused: acquire(nbytes) hands out the smallest free buffer that
+    fits (or allocates one of the next power-of-two size), release() returns
+    it.  Pinned memory lets the upload run at full PCIe speed and lets every
+    GPU read the arena directly (zero-copy) on the multi-GPU path.  When no
+    CUDA driver is present (CPU tests) it hands out plain numpy memory."""
+
+    def __init__(self, max_free: int = 4):
+        self._free: list = []
+        self._lock = threading.Lock()
+        self._max_free = max_free
+
+    def acquire(self, nbytes: int):
+        nbytes = max(int(nbytes), 1)
+        with self._lock:
+            fits = [b for b in self._free if b[1] >= nbytes]
+            if fits:
+                best = min(fits, key=lambda b: b[1])
+                self._free.remove(best)
+                ptr, cap = best
+                return PinnedBuffer(self, ptr, cap, nbytes)
+        cap = 1 << max(20, (nbytes - 1).bit_length())
+        ptr = load().sw_host_alloc(cap)
+        if not ptr:
+            return PinnedBuffer(None, None, nbytes, nbytes)    # unpinned fallback memory
+        return PinnedBuffer(self, ptr, cap, nbytes)
+
+    def _release(self, ptr, cap):
+        with self._lock:
+            self._free.append((ptr, cap))
+            while len(self._free) > self._max_free:
+                p, _ = min(self._free, key=lambda b: b[1])
+                self._free.remove((p, _))
+                load().sw_host_free(p)
+
+
+class PinnedBuffer:
+    """A pinned host buffer lent by PinnedPool; `array` is a uint8 view of
+    the requested size.  release() (or garbage collection) returns it."""
+
+    def __init__(self, pool, ptr, cap, nbytes):
+        self.pool, self.ptr, self.cap = pool, ptr, cap
+        if ptr is None:
+            self.array = np.empty(nbytes, dtype=np.uint8)
+        else:
+            self.array = np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(ptr))
+        self.pinned = ptr is not None
+
+    def release(self):
+        if self.pool is not None and self.ptr is not None:
+            pool, ptr, cap = self.pool, self.ptr, self.cap
+            self.pool = self.ptr = None
+            self.array = None
+            pool._release(ptr, cap)
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+_POOL = None
+
+
+def pinned_pool() -> PinnedPool:
+    global _POOL
+    if _POOL is None:
+        _POOL = PinnedPool()
+    return _POOL

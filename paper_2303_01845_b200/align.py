@@ -21,7 +21,8 @@ import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from time import perf_counter
-from typing import Optional, Sequence
+from collections.abc import Sequence
+from typing import Optional
 
 import numpy as np
 
@@ -67,19 +68,22 @@ class AlignParams:
             raise ValueError("substitution matrix must be symmetric")
 
 
-@dataclass(slots=True)
-class AlignmentResult:
-    """Optimal local alignment; spans are 0-based inclusive residue offsets,
-    all -1 for the empty (score 0) alignment."""
+try:  # drop-in interop: the reference's own result class when importable
+    from pastislite.align import AlignmentResult  # type: ignore  # noqa: F401
+except ImportError:  # pragma: no cover - the GPU box has no pastislite
+    @dataclass(slots=True)
+    class AlignmentResult:
+        """Optimal local alignment; spans are 0-based inclusive residue offsets,
+        all -1 for the empty (score 0) alignment (align.py:55-67)."""
 
-    score: int
-    i_begin: int
-    i_end: int
-    j_begin: int
-    j_end: int
-    matches: int
-    aln_len: int
-    cells: int
+        score: int
+        i_begin: int
+        i_end: int
+        j_begin: int
+        j_end: int
+        matches: int
+        aln_len: int
+        cells: int
 
 
 def encode(residues: str) -> np.ndarray:
@@ -123,28 +127,84 @@ def align_packed(batch: PackedBatch, params: AlignParams, devices=(0,)):
     return _native.align_multi(batch.arena, batch.pairs, p, devices)
 
 
-def _to_results(batch: PackedBatch, rec: np.ndarray):
-    """Materialise AlignmentResult objects in input order (API edge only)."""
-    results: list = [None] * batch.n_input
-    errors = list(batch.errors)
-    cells = (batch.pairs["a_len"].astype(np.int64) * batch.pairs["b_len"].astype(np.int64)).tolist()
-    rows = rec.tolist()
-    idx = batch.index.tolist()
-    n_ok = 0
-    cell_sum = 0
-    for k, (row, c) in enumerate(zip(rows, cells)):
-        status = row[7]
-        if status == _native.STATUS_OK:
-            results[idx[k]] = AlignmentResult(row[0], row[1], row[2], row[3], row[4], row[5],
-                                              row[6], c)
-            n_ok += 1
-            cell_sum += c
-        elif status == _native.STATUS_EMPTY:
-            errors.append((idx[k], AlignmentError("cannot align an empty sequence")))
+class ResultList(Sequence):
+    """The `results` list of align_batch / AlignEngine (align.py:231-246), in
+    input order: AlignmentResult or None per input pair.  The records stay a
+    RESULT_DTYPE array; an AlignmentResult is built only when an element is
+    read, so a batch of 1M pairs costs no Python objects until the caller
+    touches them (`records`, `ok` and `cells` give vectorised access)."""
+
+    __slots__ = ("records", "ok", "cells", "_n")
+
+    def __init__(self, batch: PackedBatch, rec: np.ndarray):
+        n = self._n = batch.n_input
+        ok = rec["status"] == _native.STATUS_OK
+        cells = batch.pairs["a_len"].astype(np.int64) * batch.pairs["b_len"]
+        if len(batch.index) == n:          # no packing errors: packed order == input order
+            self.records, self.ok, self.cells = rec, ok, cells
         else:
-            errors.append((idx[k], AssertionError("traceback lost at H state")))
-    errors.sort(key=lambda e: e[0])
-    return results, errors, n_ok, cell_sum
+            self.records = np.zeros(n, dtype=_native.RESULT_DTYPE)
+            self.records[batch.index] = rec
+            self.ok = np.zeros(n, dtype=bool)
+            self.ok[batch.index] = ok
+            self.cells = np.zeros(n, dtype=np.int64)
+            self.cells[batch.index] = cells
+
+    def __len__(self) -> int:
+        return self._n
+
+    def _make(self, i: int):
+        if not self.ok[i]:
+            return None
+        r = self.records[i]
+        return AlignmentResult(int(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4]), int(r[5]),
+                               int(r[6]), int(self.cells[i]))
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._make(k) for k in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("result index out of range")
+        return self._make(i)
+
+    def __iter__(self):
+        rows = self.records.tolist()
+        cells = self.cells.tolist()
+        for ok, row, c in zip(self.ok.tolist(), rows, cells):
+            yield AlignmentResult(row[0], row[1], row[2], row[3], row[4], row[5], row[6], c) \
+                if ok else None
+
+    def __eq__(self, other):
+        try:
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        except TypeError:
+            return NotImplemented
+
+    def __repr__(self) -> str:
+        return f"ResultList({len(self)} results)"
+
+
+def _to_results(batch: PackedBatch, rec: np.ndarray):
+    """(results, errors, n_ok, cells): lazy results in input order, per-pair
+    errors sorted by input index (packing errors + device status)."""
+    results = ResultList(batch, rec)
+    errors = list(batch.errors)
+    bad = np.flatnonzero(rec["status"] != _native.STATUS_OK)
+    for k in bad.tolist():
+        idx = int(batch.index[k])
+        if rec["status"][k] == _native.STATUS_EMPTY:
+            errors.append((idx, AlignmentError("cannot align an empty sequence")))
+        else:
+            errors.append((idx, AssertionError("traceback lost at H state")))
+    if len(bad):
+        errors.sort(key=lambda e: e[0])
+    ok = results.ok
+    if not len(bad) and len(batch.index) == batch.n_input:
+        return results, errors, batch.n_input, int(results.cells.sum())
+    return results, errors, int(ok.sum()), int(results.cells[ok].sum())
 
 
 def smith_waterman(a: str, b: str, params: AlignParams) -> AlignmentResult:
@@ -182,26 +242,46 @@ def evaluate_pair(
     return None
 
 
-@dataclass
-class BatchCounters:
-    alignments: int = 0
-    cells: int = 0
-    kernel_seconds: float = 0.0
+try:  # drop-in interop: the reference's counters class when importable
+    from pastislite.align import BatchCounters  # type: ignore  # noqa: F401
+except ImportError:  # pragma: no cover
+    @dataclass
+    class BatchCounters:
+        alignments: int = 0
+        cells: int = 0
+        kernel_seconds: float = 0.0
 
-    def merge(self, other: "BatchCounters") -> None:
-        self.alignments += other.alignments
-        self.cells += other.cells
-        self.kernel_seconds += other.kernel_seconds
+        def merge(self, other: "BatchCounters") -> None:
+            self.alignments += other.alignments
+            self.cells += other.cells
+            self.kernel_seconds += other.kernel_seconds
 
 
 def _align(pairs: Sequence[tuple], params: AlignParams, devices) -> tuple:
-    batch = pack_pairs(pairs)
-    rec, timings = align_packed(batch, params, devices)
+    t0 = perf_counter()
+    pool = _native.pinned_pool()
+    bufs = []
+
+    def alloc(nbytes):
+        b = pool.acquire(nbytes)
+        bufs.append(b)
+        return b.array
+
+    try:
+        batch = pack_pairs(pairs, alloc=alloc)
+        t1 = perf_counter()
+        rec, timings = align_packed(batch, params, devices)
+    finally:
+        for b in bufs:
+            b.release()
+    t2 = perf_counter()
     results, errors, n_ok, cell_sum = _to_results(batch, rec)
+    t3 = perf_counter()
     # kernel_seconds = forward fill time, the quantity align.py:103-122 times
     fwd = sum(t["forward_ms"] for t in timings) / 1e3
     counters = BatchCounters(alignments=n_ok, cells=cell_sum, kernel_seconds=fwd)
-    return results, errors, counters, timings
+    phases = {"pack": t1 - t0, "align": t2 - t1, "results": t3 - t2}
+    return results, errors, counters, timings, phases
 
 
 def align_batch(pairs: Sequence[tuple], params: AlignParams) -> tuple:
@@ -209,7 +289,7 @@ def align_batch(pairs: Sequence[tuple], params: AlignParams) -> tuple:
 
     Returns (results, errors, counters); a failing pair leaves None in its
     result slot and an (index, exception) entry instead of aborting."""
-    results, errors, counters, _ = _align(pairs, params, _device_ids(1))
+    results, errors, counters, _, _ = _align(pairs, params, _device_ids(1))
     return results, errors, counters
 
 
@@ -243,6 +323,7 @@ class AlignEngine:
         self._pool: Optional[ThreadPoolExecutor] = None
         self._devices: Optional[list] = None
         self._lock = threading.Lock()
+        self.last_phases: dict = {}   # host pack / device align / results seconds, last batch
 
     def start(self) -> None:
         if self._devices is None:
@@ -253,7 +334,9 @@ class AlignEngine:
     def _run(self, pairs: list) -> tuple:
         t0 = perf_counter()
         with self._lock:
-            results, errors, counters, timings = _align(pairs, self.params, self._devices)
+            results, errors, counters, timings, phases = _align(pairs, self.params,
+                                                                self._devices)
+            self.last_phases = phases
         wall = perf_counter() - t0
         if len(timings) <= 1:
             lanes = [(self._devices[0], counters.kernel_seconds, wall)]

@@ -2,29 +2,44 @@
 
 The reference hands each worker pickled (str, str, payload) tuples
 (pipeline.py:307 -> AlignEngine.submit, align.py:327-335).  Here a batch is
-packed once into
-  * a flat uint8 arena holding every DISTINCT sequence once (the pipeline
-    reuses `residues[i]` objects across pairs, so sequences are deduplicated
-    by object identity first and by value second), raw ASCII bytes exactly as
-    the reference receives them, and
+packed once, by the C extension `_pack` (csrc/pack_ext.c), into
+  * a flat uint8 arena holding every DISTINCT sequence object once (the
+    pipeline reuses `residues[i]` objects across pairs, so sequences are
+    deduplicated by object identity), raw ASCII bytes exactly as the
+    reference receives them, in a caller-chosen buffer (the engine passes
+    recycled pinned host memory, so the upload runs at full PCIe speed and
+    several GPUs can read it directly), and
   * a pair table (a_off, b_off, a_len, b_len) in input order (sw_pair_t).
-Length binning and cell-balanced sharding happen on the device / in the C++
-host driver (sw_engine.cu), so they never reorder results.
+Length binning and cell-balanced sharding happen on the device, so they
+never reorder results.
 
-Per-pair input errors are detected here with the reference's order and
-exception types (align.py:81-84): empty -> AlignmentError, then str.encode
-("ascii") errors (UnicodeEncodeError) for a, then b.
+Per-pair input errors are detected with the reference's order and exception
+types (align.py:81-84): empty -> AlignmentError, then str.encode("ascii")
+errors (UnicodeEncodeError) for a, then b; sequences over 65,000 residues
+(the GPU aligner's domain) -> ValueError.  A failing pair is reported in
+`errors` and left out of the table; the rest of the batch proceeds.
 """
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from ._native import PAIR_DTYPE
 
+try:  # drop-in interop: the reference's own exception class when importable
+    from pastislite.align import AlignmentError  # type: ignore  # noqa: F401
+except ImportError:  # pragma: no cover - the GPU box has no pastislite
+    class AlignmentError(ValueError):
+        """Same role as pastislite.align.AlignmentError (align.py:33-34)."""
 
-class AlignmentError(ValueError):
-    """Same role as pastislite.align.AlignmentError (align.py:33-34)."""
+try:
+    from . import _pack
+except ImportError as exc:  # built by __graft_entry__.build() / build.build_pack()
+    raise ImportError("paper_2303_01845_b200._pack is not built: run "
+                      "python -c 'import __graft_entry__ as g; g.build()'") from exc
+
+_THREADS = max(1, min(16, len(os.sched_getaffinity(0))))
 
 
 @dataclass
@@ -34,6 +49,7 @@ class PackedBatch:
     index: np.ndarray                      # int64, packed row -> input position
     n_input: int                           # number of input pairs
     errors: list = field(default_factory=list)  # [(input index, exception)]
+    buffer: object = None                  # owner of `arena` (pinned pool slot) or None
 
     @property
     def cells(self) -> int:
@@ -41,60 +57,31 @@ class PackedBatch:
         return int(np.dot(p["a_len"].astype(np.uint64), p["b_len"].astype(np.uint64)))
 
 
-def pack_pairs(pairs) -> PackedBatch:
-    """Pack (a, b[, payload]) items; invalid pairs are reported, not packed."""
+def _numpy_alloc(nbytes: int) -> np.ndarray:
+    return np.empty(nbytes, dtype=np.uint8)
+
+
+def pack_pairs(pairs, alloc=None) -> PackedBatch:
+    """Pack (a, b[, payload]) items; invalid pairs are reported, not packed.
+
+    `alloc(nbytes)` returns the writable arena buffer (default: a new numpy
+    array); it is called once, after the table is known."""
     n = len(pairs)
-    by_id: dict = {}
-    by_val: dict = {}
-    chunks: list = []
-    offset = 0
-    a_off = np.empty(n, dtype=np.uint64)
-    b_off = np.empty(n, dtype=np.uint64)
-    a_len = np.empty(n, dtype=np.uint32)
-    b_len = np.empty(n, dtype=np.uint32)
-    keep = np.ones(n, dtype=bool)
-    errors = []
+    table = np.empty(n, dtype=PAIR_DTYPE)
+    index = np.empty(n, dtype=np.int64)
+    holder = {}
 
-    def place(s):
-        nonlocal offset
-        key = id(s)
-        hit = by_id.get(key)
-        if hit is not None and hit[0] is s:
-            return hit[1]
-        o = by_val.get(s)
-        if o is None:
-            raw = s.encode("ascii")
-            o = offset
-            chunks.append(raw)
-            offset += len(raw)
-            by_val[s] = o
-        by_id[key] = (s, o)
-        return o
+    def _alloc(nbytes):
+        buf = (alloc or _numpy_alloc)(nbytes)
+        holder["buf"] = buf
+        return buf
 
-    for idx, item in enumerate(pairs):
-        a, b = item[0], item[1]
-        try:
-            if not a or not b:
-                raise AlignmentError("cannot align an empty sequence")
-            oa = place(a)
-            ob = place(b)
-        except Exception as exc:  # noqa: BLE001 - per-pair isolation (align.py:236-241)
-            keep[idx] = False
-            errors.append((idx, exc))
-            continue
-        a_off[idx] = oa
-        b_off[idx] = ob
-        a_len[idx] = len(a)
-        b_len[idx] = len(b)
-
-    arena = np.frombuffer(b"".join(chunks) or b"\0", dtype=np.uint8)
-    index = np.flatnonzero(keep).astype(np.int64)
-    table = np.empty(len(index), dtype=PAIR_DTYPE)
-    table["a_off"] = a_off[index]
-    table["b_off"] = b_off[index]
-    table["a_len"] = a_len[index]
-    table["b_len"] = b_len[index]
-    return PackedBatch(arena=arena, pairs=table, index=index, n_input=n, errors=errors)
+    kept, arena, nbytes, errors = _pack.pack(pairs, table, index, _alloc, AlignmentError,
+                                             _THREADS)
+    arena = np.frombuffer(arena, dtype=np.uint8, count=max(int(nbytes), 1)) \
+        if not isinstance(arena, np.ndarray) else arena[: max(int(nbytes), 1)]
+    return PackedBatch(arena=arena, pairs=table[:kept], index=index[:kept], n_input=n,
+                       errors=errors, buffer=holder.get("buf"))
 
 
 def pack_codes(seqs_a, seqs_b) -> tuple:

@@ -38,6 +38,23 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def pack_ext_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_pack" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pack(force: bool = False) -> str:
+    """The drop-in API's packing layer (csrc/pack_ext.c, a CPython extension)."""
+    import sysconfig
+    target = pack_ext_path()
+    src = os.path.join(CSRC, "pack_ext.c")
+    if force or _stale(target, [src]):
+        cc = os.environ.get("CC", "gcc")
+        subprocess.run([cc, "-O2", "-fPIC", "-shared", "-pthread", "-Wall",
+                        "-I", sysconfig.get_paths()["include"], "-o", target, src], check=True)
+    return target
+
+
 def build_oracle(force: bool = False) -> str:
     odir = os.path.join(ROOT, "oracle")
     target = os.path.join(odir, "liborc.so")
@@ -58,5 +75,6 @@ def build_synth(force: bool = False) -> str:
 if __name__ == "__main__":
     force = "--force" in sys.argv
     print(build_native(force=force, verbose="-v" in sys.argv))
+    print(build_pack(force=force))
     print(build_oracle(force=force))
     print(build_synth(force=force))

@@ -14,16 +14,19 @@ from dataclasses import dataclass
 import numpy as np
 
 
-@dataclass(slots=True)
-class SimilarityEdge:
-    """Canonical undirected edge: i < j, fractions in [0, 1]."""
+try:  # drop-in interop: the reference's own edge class when importable
+    from pastislite.seqio import SimilarityEdge  # type: ignore  # noqa: F401
+except ImportError:  # pragma: no cover - the GPU box has no pastislite
+    @dataclass(slots=True)
+    class SimilarityEdge:
+        """Canonical undirected edge: i < j, fractions in [0, 1]."""
 
-    i: int
-    j: int
-    score: int
-    identity: float
-    coverage_i: float
-    coverage_j: float
+        i: int
+        j: int
+        score: int
+        identity: float
+        coverage_i: float
+        coverage_j: float
 
 
 def format_edge_line(edge: SimilarityEdge, headers) -> str:

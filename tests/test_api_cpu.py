@@ -1,11 +1,12 @@
 """Host-side API parity with the reference (no GPU needed)."""
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
-from conftest import FIELDS, load_golden, matrix
+from conftest import FIELDS, ROOT, load_golden, matrix
 import paper_2303_01845_b200 as sw
 from paper_2303_01845_b200 import alphabet, blosum62
 
@@ -126,3 +127,79 @@ def test_pack_codes_layout():
     assert bytes(arena) == b"AAAGGCTTTT"
     assert t["a_off"].tolist() == [0, 5] and t["b_off"].tolist() == [3, 6]
     assert t["a_len"].tolist() == [3, 1] and t["b_len"].tolist() == [2, 4]
+
+
+def test_pack_pairs_parallel_path_matches_sequential_semantics():
+    """The C packer's threaded fast path (tuples of ASCII str) and its Python-
+    semantics path (everything else) give the same table: every packed pair
+    points at its own bytes, shared objects are stored once, and the per-pair
+    errors keep the reference's types and input order."""
+    rng = np.random.default_rng(3)
+    seqs = ["".join(rng.choice(list("ACDEFGHIKLMNPQRSTVWY"), size=int(n)))
+            for n in rng.integers(1, 400, size=500)]
+    pairs = []
+    for k in range(20000):
+        a, b = seqs[k % 500], seqs[(k * 7 + 3) % 500]
+        if k % 997 == 5:
+            pairs.append((a, "", k))                 # AlignmentError
+        elif k % 991 == 7:
+            pairs.append([a, b])                     # list item: slow path, still packed
+        elif k % 983 == 11:
+            pairs.append((a, "A" * 65001, k))        # over the GPU domain: ValueError
+        elif k % 977 == 13:
+            pairs.append((a, b.encode(), k))         # bytes: AttributeError like .encode
+        else:
+            pairs.append((a, b, k))
+    batch = sw.pack_pairs(pairs)
+    err_idx = [e[0] for e in batch.errors]
+    assert err_idx == sorted(err_idx)
+    kinds = {k: type(e) for k, e in batch.errors}
+    for k in err_idx:
+        assert kinds[k] in (sw.AlignmentError, ValueError, AttributeError)
+    assert len(batch.index) + len(batch.errors) == len(pairs)
+    raw = bytes(batch.arena)
+    for row, k in zip(batch.pairs.tolist(), batch.index.tolist()):
+        a_off, b_off, la, lb = row
+        assert raw[a_off:a_off + la].decode() == pairs[k][0]
+        assert raw[b_off:b_off + lb].decode() == pairs[k][1]
+    assert len(raw) <= sum(len(s) for s in seqs) + 65001   # distinct objects stored once
+
+
+def test_result_list_is_lazy_and_list_like():
+    from paper_2303_01845_b200 import _native
+    from paper_2303_01845_b200.align import ResultList
+    batch = sw.pack_pairs([("AAAA", "AAAA", 0), ("", "A", 1), ("MKV", "MKV", 2)])
+    rec = np.zeros(2, dtype=_native.RESULT_DTYPE)
+    rec["score"] = [16, 15]
+    rec["aln_len"] = [4, 3]
+    res = ResultList(batch, rec)
+    assert len(res) == 3 and res[1] is None
+    assert res[0].score == 16 and res[0].cells == 16 and res[-1].cells == 9
+    assert [r.score if r else None for r in res] == [16, None, 15]
+    assert res[0:2] == [res[0], None]
+    assert list(res) == list(res[:])
+
+
+def test_interop_with_reference_classes_when_importable():
+    """With pastislite importable (this container), the drop-in uses the
+    reference's own AlignmentError / AlignmentResult / BatchCounters /
+    SimilarityEdge classes, so `except pastislite.align.AlignmentError` and
+    dataclass equality work across the two packages."""
+    import subprocess
+    import sys
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present")
+    code = (f"import sys; sys.path[:0] = [{ref!r}, {ROOT!r}]\n"
+            "import pastislite.align as R, pastislite.seqio as S\n"
+            "import paper_2303_01845_b200 as sw\n"
+            "from paper_2303_01845_b200 import edges\n"
+            "assert sw.AlignmentError is R.AlignmentError\n"
+            "assert sw.AlignmentResult is R.AlignmentResult\n"
+            "assert sw.BatchCounters is R.BatchCounters\n"
+            "assert edges.SimilarityEdge is S.SimilarityEdge\n"
+            "b = sw.pack_pairs([('', 'A', 0)])\n"
+            "assert isinstance(b.errors[0][1], R.AlignmentError)\n"
+            "print('ok')\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
