@@ -363,15 +363,23 @@ def main():
         pins.append(ptr)
         return arr
 
-    # this rank's batch, generated straight into pinned host memory
-    arena_np, table_np = make_batch(args.workload, args.pairs, 2303 + rank, alloc=alloc)
-    cells = int(np.dot(table_np["a_len"].astype(np.int64), table_np["b_len"].astype(np.int64)))
-    n_pairs = len(table_np)
+    # The batch, generated straight into pinned host memory.  N = 1: the
+    # config's pairs.  N > 1 (weak scaling): a global batch of N x that many
+    # pairs (the first N x pairs of the same seeded stream) held by every
+    # rank, as the node's host memory would hold it; each GPU plans the
+    # cell-balanced partition on the device and takes its shard
+    # (sw_align_shard), and the result records are gathered to rank 0 over
+    # NCCL -- all inside the timed region.
+    arena_np, table_np = make_batch(args.workload, args.pairs * world, 2303, alloc=alloc)
+    cells_all = int(np.dot(table_np["a_len"].astype(np.int64), table_np["b_len"].astype(np.int64)))
+    n_all = len(table_np)
+    n_local = _native.shard_count(n_all, world, rank)
 
     # device-resident inputs for `value`
     d_arena = torch.from_numpy(arena_np).to(dev)
     d_pairs = torch.from_numpy(table_np.view(np.uint8).copy()).to(dev)
-    d_out = torch.empty(n_pairs * 32, dtype=torch.uint8, device=dev)
+    d_out = torch.empty(max(n_local, 1) * 32, dtype=torch.uint8, device=dev)
+    d_idx = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
@@ -379,20 +387,33 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    def max_over_ranks(x: float) -> float:
+    def max_over_ranks(xs):
         if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+            return list(xs)
+        t = torch.tensor(list(xs), dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return t.cpu().tolist()
+
+    def gather_to_rank0(d_rec, d_ix):
+        from paper_2303_01845_b200.distributed import gather_rows
+        rows = torch.empty((n_local, 9), dtype=torch.int32, device=dev)
+        rows[:, :8] = d_rec.view(torch.int32)[: n_local * 8].view(n_local, 8)
+        rows[:, 8] = d_ix[:n_local]
+        return gather_rows(rows, n_all, rank, world, dst=0)
 
     def device_step():
-        return _native.align_device(d_arena.data_ptr(), arena_np.size, d_pairs.data_ptr(),
-                                    n_pairs, params, d_out.data_ptr(), device=local,
-                                    stream=stream.cuda_stream)
+        if world == 1:
+            return _native.align_device(d_arena.data_ptr(), arena_np.size, d_pairs.data_ptr(),
+                                        n_all, params, d_out.data_ptr(), device=local,
+                                        stream=stream.cuda_stream), None
+        tm = _native.align_shard(d_arena.data_ptr(), arena_np.size, d_pairs.data_ptr(), n_all,
+                                 rank, world, params, d_out.data_ptr(), d_idx.data_ptr(),
+                                 device=local, stream=stream.cuda_stream)
+        return tm, gather_to_rank0(d_out, d_idx)
 
     step_ms, launches = [], 0
     tms = []
+    gathered = None
     with ClockSampler(local) as clocks:
         # warm-up also lets the first clock query (which stalls the driver
         # briefly) happen before the timed region
@@ -409,21 +430,22 @@ def main():
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
+                barrier()
                 e0.record(stream)
-                tm = device_step()
+                tm, gathered = device_step()
                 e1.record(stream)
                 torch.cuda.synchronize()
                 step_ms.append(e0.elapsed_time(e1))
                 tms.append(tm)
                 launches += tm["launches"]
         barrier()
-    dev_ms = max_over_ranks(float(np.sum(step_ms)))
-    total_cells = cells * world * args.steps
+    dev_ms = float(np.sum(max_over_ranks(step_ms)))
+    total_cells = cells_all * args.steps
     value = total_cells / (dev_ms / 1e3) / 1e9
-    rec_dev = d_out.cpu().numpy().view(_native.RESULT_DTYPE)
+    rec_dev = (d_out.cpu().numpy().view(_native.RESULT_DTYPE)[:n_all] if world == 1 else gathered)
 
     # end to end through the host C-ABI call with pinned buffers
-    po_ptr, po = pinned(n_pairs * 32)
+    po_ptr, po = pinned(n_all * 32)
     pins.append(po_ptr)
     pp_ptr, pp = pinned(table_np.nbytes)
     pins.append(pp_ptr)
@@ -433,27 +455,40 @@ def main():
 
     def host_step():
         t0 = time.perf_counter()
-        _, t = _native.align_host(arena_np, host_pairs, params, device=local, out=host_out)
-        return (time.perf_counter() - t0) * 1e3, t
+        if world == 1:
+            _native.align_host(arena_np, host_pairs, params, device=local, out=host_out)
+            res = host_out
+        else:
+            _native.align_shard(arena_np.ctypes.data, arena_np.size, host_pairs.ctypes.data, n_all,
+                                rank, world, params, d_out.data_ptr(), d_idx.data_ptr(),
+                                device=local, stream=stream.cuda_stream)
+            res = gather_to_rank0(d_out, d_idx)      # records land on rank 0's host
+        return (time.perf_counter() - t0) * 1e3, res
 
     for _ in range(max(1, args.warmup)):
         host_step()
     barrier()
     e2e_ms = []
+    res_host = None
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
-        ms, _ = host_step()
+        barrier()
+        ms, res_host = host_step()
         e2e_ms.append(ms)
     barrier()
-    e2e_total = max_over_ranks(float(np.sum(e2e_ms)))
+    e2e_total = float(np.sum(max_over_ranks(e2e_ms)))
     e2e_value = total_cells / (e2e_total / 1e3) / 1e9
-    ok = bool((host_out["status"] == 0).all()) and bool((host_out == rec_dev).all())
+    ok = True
+    if rank == 0:
+        ok = bool((res_host["status"] == 0).all()) and bool((res_host == rec_dev).all())
+    cells = cells_all // world
+    n_pairs = n_all // world
 
     # end to end through the reference-shaped Python API
     api = None
     if not args.no_api and world == 1:
-        api = api_leg(args, arena_np, table_np, cells, flush, torch)
+        api = api_leg(args, arena_np, table_np, cells_all, flush, torch)
 
     if rank != 0:
         if world > 1:
@@ -474,12 +509,12 @@ def main():
     peak_gcups = sms * clk_ghz * 4 * 32 * 2 / slots_per_word
     mean = lambda key: float(np.mean([t[key] for t in tms]))  # noqa: E731
     fwd_ms = mean("forward_ms")
-    fwd_gcups = cells / (fwd_ms / 1e3) / 1e9
+    fwd_gcups = (cells_all if world == 1 else mean("cells")) / (fwd_ms / 1e3) / 1e9
     dominant = ("k_score_cta_packed<8> (K1cp: forward, 2 long pairs per CTA)"
                 if args.workload == "config5" else
                 "k_score_packed<R> (K1p: forward, 2 pairs per warp, R = 4..16 rows/lane "
                 "classes running concurrently)")
-    cc = computed_cells(table_np)
+    cc = computed_cells(table_np[: args.pairs])
     line = {
         "metric": metric_of(args.workload),
         "value": value,
@@ -493,7 +528,7 @@ def main():
         "vs_baseline": None,
         "dtype": DTYPE,
         "data": "synthetic",
-        "alignments_per_sec": n_pairs * world * args.steps / (dev_ms / 1e3),
+        "alignments_per_sec": n_all * args.steps / (dev_ms / 1e3),
         "forward_gcups": fwd_gcups,
         "phase_ms_per_step": {
             "forward": fwd_ms,
@@ -510,8 +545,14 @@ def main():
         "results_ok": ok,
         "config": {"workload": WORKLOADS[args.workload]["desc"],
                    "pairs_per_gpu": n_pairs, "cells_per_gpu_per_step": cells,
+                   "global_pairs": n_all, "global_cells_per_step": cells_all,
                    "l2": "flushed between timed steps (256 MiB memset, outside the events)",
-                   "parallelism": f"one process per GPU x{world}, weak scaling"},
+                   "parallelism": (f"one process per GPU x{world}, weak scaling: a global batch "
+                                   f"of {world} x {args.pairs} pairs held by every rank; "
+                                   "device-planned cell-balanced snake partition "
+                                   "(sw_align_shard), NCCL gather of the result records to "
+                                   "rank 0, all inside the timed region")
+                   if world > 1 else "1 GPU"},
         "roofline": {"bound": "int-issue", "kernel": dominant,
                      "achieved": fwd_gcups, "peak": peak_gcups, "unit": "GCUPS",
                      "frac": fwd_gcups / peak_gcups,
@@ -521,16 +562,19 @@ def main():
                                    f"(u16x2) / {slots_per_word:.0f} issue slots per packed Gotoh "
                                    "cell (4 adds + 5 maxes); pipe rates measured in tools/microbench",
                      "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 56/(m*n) "
-                                 f"= {(arena_np.size + 56 * n_pairs) / cells:.4f} B -> non-binding",
+                                 f"= {(arena_np.size + 56 * n_all) / cells_all:.4f} B -> non-binding",
                      "alu_pipe_ceiling": sms * clk_ghz * 4 * 64 / 11.0,
                      **cc,
                      **ncu_fields(args.workload, dev_ms / args.steps)},
         "e2e": {"value": e2e_value, "unit": "GCUPS",
-                "h2d_bytes_per_step": int(arena_np.size + table_np.nbytes),
-                "d2h_bytes_per_step": int(n_pairs * 32),
+                "h2d_bytes_per_step": int(arena_np.size + table_np.nbytes) if world == 1 else
+                int(table_np.nbytes * world + arena_np.size),
+                "d2h_bytes_per_step": int(n_all * 32),
                 "ms_per_step": e2e_total / args.steps,
-                "alignments_per_sec": n_pairs * world * args.steps / (e2e_total / 1e3),
-                "entry": "sw_align_batch (C ABI, pinned host buffers)"},
+                "alignments_per_sec": n_all * args.steps / (e2e_total / 1e3),
+                "entry": "sw_align_batch (C ABI, pinned host buffers)" if world == 1 else
+                "sw_align_shard per rank (pinned host arena read zero-copy, only the shard's "
+                "bytes) + NCCL gather of the records to rank 0 + D2H there"},
         "gpu_launches": int(launches),
         "clocks": csum,
     }

@@ -122,25 +122,46 @@ int sw_align_batch(int device, const uint8_t *arena, uint64_t arena_bytes,
 
 /* Same on DEVICE-resident buffers (arena, pairs and out all on `device`).
  * `stream` is a cudaStream_t (NULL = the library's own stream).  Returns
- * after the work completes. */
+ * after the work completes.  The arena may start at any byte address. */
 int sw_align_batch_device(int device, const uint8_t *d_arena, uint64_t arena_bytes,
                           const sw_pair_t *d_pairs, uint64_t n_pairs,
                           const sw_params_t *params, sw_result_t *d_out, void *stream,
                           sw_timing_t *timing);
 
-/* Shard a HOST batch over n_devices GPUs by cell count (|a|*|b|, greedy
- * least-loaded), run every shard concurrently (one host thread per GPU),
- * gather results into `out` in input order.  per_device_timing may be NULL
+/* Shard a HOST batch over n_devices GPUs by cell count and gather the
+ * results into `out` in input order (replaces AlignEngine's process lanes,
+ * align.py:299-335, whose _chunk split align.py:265-269 ignores lengths).
+ * Every GPU plans the same partition on the device (sw_align_shard), reads
+ * ONLY its shard's sequence bytes straight from the host arena (pinned
+ * memory: zero-copy over PCIe; pageable memory is registered for the call)
+ * and aligns them; one host thread per GPU.  per_device_timing may be NULL
  * or point to n_devices entries. */
 int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena,
                          uint64_t arena_bytes, const sw_pair_t *pairs, uint64_t n_pairs,
                          const sw_params_t *params, sw_result_t *out,
                          sw_timing_t *per_device_timing);
 
-/* Cell-balanced partition used by sw_align_batch_multi, exposed for the host
- * driver and its tests: writes shard[k] in [0, n_shards) for every pair
- * (LPT: pairs in descending a_len*b_len order go to the least-loaded shard).
- * load[s] (may be NULL) receives the cell total of shard s. */
+/* One shard of a cell-balanced partition, planned on `device` (the unit of
+ * the multi-process driver: one process per GPU, each calling this with its
+ * rank, then gathering the records over NCCL).  The plan: pairs in stable
+ * descending a_len*b_len order, dealt to the shards in a snake (sorted
+ * position r*n_shards + q goes to shard q in even rounds, n_shards-1-q in odd
+ * ones), so every shard's cells are within one pair of every other's.
+ * `arena` and `pairs` may be device memory or host memory (pinned host
+ * memory is read zero-copy); d_out / d_index are DEVICE buffers of
+ * sw_shard_count(n_pairs, n_shards, shard) entries receiving the shard's
+ * results and their input positions. */
+int sw_align_shard(int device, const uint8_t *arena, uint64_t arena_bytes,
+                   const sw_pair_t *pairs, uint64_t n_pairs, int shard, int n_shards,
+                   const sw_params_t *params, sw_result_t *d_out, uint32_t *d_index,
+                   void *stream, sw_timing_t *timing);
+
+/* Pairs shard `shard` of `n_shards` receives from a batch of n_pairs. */
+uint64_t sw_shard_count(uint64_t n_pairs, int n_shards, int shard);
+
+/* The same partition computed on the host (for host drivers and tests):
+ * shard[k] in [0, n_shards) for every pair; load[s] (may be NULL) receives
+ * the cell total of shard s. */
 int sw_partition_pairs(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards,
                        int32_t *shard, uint64_t *load);
 

@@ -43,6 +43,8 @@ EXPORTED_SYMBOLS = (
     "sw_align_batch_device",
     "sw_align_batch_multi",
     "sw_partition_pairs",
+    "sw_align_shard",
+    "sw_shard_count",
     "sw_release",
     "sw_host_alloc",
     "sw_host_free",
@@ -142,6 +144,11 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
         lib.sw_align_batch_multi.restype = i32
         lib.sw_align_batch_multi.argtypes = [i32, vp, vp, u64, vp, u64,
                                              ctypes.POINTER(SwParams), vp, vp]
+        lib.sw_align_shard.restype = i32
+        lib.sw_align_shard.argtypes = [i32, vp, u64, vp, u64, i32, i32, ctypes.POINTER(SwParams),
+                                       vp, vp, vp, ctypes.POINTER(SwTiming)]
+        lib.sw_shard_count.restype = u64
+        lib.sw_shard_count.argtypes = [u64, i32, i32]
         lib.sw_partition_pairs.restype = i32
         lib.sw_partition_pairs.argtypes = [vp, u64, i32, vp, vp]
         lib.sw_release.restype = None
@@ -226,8 +233,25 @@ def align_device(d_arena: int, arena_bytes: int, d_pairs: int, n_pairs: int, par
     return tm.as_dict()
 
 
+def shard_count(n_pairs: int, n_shards: int, shard: int) -> int:
+    return int(load().sw_shard_count(n_pairs, n_shards, shard))
+
+
+def align_shard(arena_ptr: int, arena_bytes: int, pairs_ptr: int, n_pairs: int, shard: int,
+                n_shards: int, params: SwParams, d_out: int, d_index: int, device: int = 0,
+                stream: int = 0) -> dict:
+    """sw_align_shard: shard `shard` of a batch (arena / pairs: device or host
+    pointers) into the DEVICE buffers d_out (results) and d_index (uint32
+    input positions)."""
+    tm = SwTiming()
+    _check(load().sw_align_shard(device, arena_ptr, arena_bytes, pairs_ptr, n_pairs, shard,
+                                 n_shards, ctypes.byref(params), d_out, d_index, stream or None,
+                                 ctypes.byref(tm)))
+    return tm.as_dict()
+
+
 def partition(pairs: np.ndarray, n_shards: int):
-    """sw_partition_pairs: LPT cell-balanced shard assignment (host only)."""
+    """sw_partition_pairs: the cell-balanced snake partition, on the host."""
     lib = load()
     pairs = np.ascontiguousarray(pairs, dtype=PAIR_DTYPE)
     shard = np.empty(len(pairs), dtype=np.int32)

@@ -34,6 +34,7 @@
 #include "sw_cta_packed.cuh"
 #include "sw_fasta.h"
 #include "sw_kmer.cuh"
+#include "sw_shard.cuh"
 
 using namespace pastis;
 
@@ -89,6 +90,9 @@ struct DeviceCtx {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   DevBuf arena, codes, pairs, out, st, lists, ctrs, stats, mat, lut, bnd, pool;
+  // sharding (sw_align_shard / sw_align_batch_multi): the whole pair table,
+  // sort keys, the shard's pair table / indices / lengths / offsets, its arena
+  DevBuf sh_pairs, sh_keys, sh_lpairs, sh_lidx, sh_llen, sh_loff, sh_arena, sh_out;
   DevBuf skeys, svals, cubtmp;  // work-list sort
   DevBuf km_arena, km_off, km_len, km_base, km_keys, km_runs, km_pairs, km_out, km_small;
   cudaEvent_t ev[16];
@@ -688,6 +692,110 @@ int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_
   return SW_OK;
 }
 
+// A caller's arena as a pointer the device can read: device memory as is,
+// pinned host memory through its mapped device address; pageable host memory
+// is registered (mapped, read-only) for the duration of the call.
+struct DeviceView {
+  const uint8_t *ptr = nullptr;
+  void *registered = nullptr;
+  int init(const void *host_or_dev, uint64_t bytes) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, host_or_dev) != cudaSuccess) {
+      cudaGetLastError();
+      at.type = cudaMemoryTypeUnregistered;
+    }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+      ptr = (const uint8_t *)host_or_dev;
+      return SW_OK;
+    }
+    if (at.type == cudaMemoryTypeUnregistered) {
+      CU(cudaHostRegister(const_cast<void *>(host_or_dev), std::max<uint64_t>(bytes, 1),
+                          cudaHostRegisterPortable | cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+      registered = const_cast<void *>(host_or_dev);
+    }
+    void *d = nullptr;
+    CU(cudaHostGetDevicePointer(&d, const_cast<void *>(host_or_dev), 0));
+    ptr = (const uint8_t *)d;
+    return SW_OK;
+  }
+  ~DeviceView() {
+    if (registered) cudaHostUnregister(registered);
+  }
+};
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Shard `shard` of `n_shards` of a batch on device c (caller holds c->mu and
+// has set the device): plan on the device (sw_shard.cuh), gather the shard's
+// sequences from `arena` (device-readable: device memory or mapped pinned
+// host memory), align them.  Writes the shard's results to d_lout and their
+// input indices to d_lidx (shard_count entries each).
+int shard_run(DeviceCtx *c, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
+              uint64_t n_pairs, int shard, int n_shards, const sw_params_t *prm,
+              sw_result_t *d_lout, uint32_t *d_lidx, cudaStream_t s, sw_timing_t *tm) {
+  if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
+  const uint64_t nl = shard_count(n_pairs, n_shards, shard);
+  if (nl == 0) return SW_OK;
+  uint32_t launches = 0;
+  // the whole table on the device (the plan needs every pair's cells)
+  const sw_pair_t *d_pairs = pairs;
+  if (!is_device_ptr(pairs)) {
+    CU(c->sh_pairs.ensure(n_pairs * sizeof(sw_pair_t)));
+    CU(cudaMemcpyAsync(c->sh_pairs.p, pairs, n_pairs * sizeof(sw_pair_t), cudaMemcpyHostToDevice, s));
+    d_pairs = (const sw_pair_t *)c->sh_pairs.p;
+  }
+  CU(c->sh_keys.ensure(4 * n_pairs * sizeof(uint32_t)));
+  uint32_t *k_in = (uint32_t *)c->sh_keys.p, *k_out = k_in + n_pairs;
+  uint32_t *v_in = k_out + n_pairs, *v_out = v_in + n_pairs;
+  k_shard_keys<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(d_pairs, n_pairs, k_in, v_in);
+  ++launches;
+  CU(cudaGetLastError());
+  size_t tmp_bytes = 0;
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out, (int)n_pairs, 0, 32, s));
+  CU(c->cubtmp.ensure(tmp_bytes));
+  CU(cub::DeviceRadixSort::SortPairs(c->cubtmp.p, tmp_bytes, k_in, k_out, v_in, v_out, (int)n_pairs, 0, 32, s));
+  launches += 5;
+  CU(c->sh_lpairs.ensure(nl * sizeof(sw_pair_t)));
+  CU(c->sh_llen.ensure(nl * sizeof(uint64_t)));
+  CU(c->sh_loff.ensure(nl * sizeof(uint64_t) + 16));
+  sw_pair_t *lpairs = (sw_pair_t *)c->sh_lpairs.p;
+  uint64_t *llen = (uint64_t *)c->sh_llen.p, *loff = (uint64_t *)c->sh_loff.p;
+  k_shard_select<<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(v_out, d_pairs, n_shards, shard, nl,
+                                                             lpairs, d_lidx, llen);
+  ++launches;
+  CU(cudaGetLastError());
+  tmp_bytes = 0;
+  CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, llen, loff, (int)nl, s));
+  CU(c->cubtmp.ensure(tmp_bytes));
+  CU(cub::DeviceScan::ExclusiveSum(c->cubtmp.p, tmp_bytes, llen, loff, (int)nl, s));
+  launches += 2;
+  uint64_t last[2] = {0, 0};
+  CU(cudaMemcpyAsync(&last[0], loff + nl - 1, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&last[1], llen + nl - 1, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const uint64_t local_bytes = last[0] + last[1];
+  CU(c->sh_arena.ensure(local_bytes + 64));
+  {
+    const unsigned blocks = (unsigned)std::min<uint64_t>((nl + 7) / 8, (uint64_t)c->sms * 16);
+    k_shard_gather<<<blocks, 256, 0, s>>>(arena, arena_bytes, lpairs, loff, nl,
+                                          (uint8_t *)c->sh_arena.p, local_bytes);
+    ++launches;
+    CU(cudaGetLastError());
+  }
+  int rc = run_device(c, (const uint8_t *)c->sh_arena.p, std::max<uint64_t>(local_bytes, 1), lpairs,
+                      nl, prm, d_lout, s, tm);
+  if (rc) return rc;
+  if (tm) tm->launches += launches;
+  return SW_OK;
+}
+
 struct Square {
   __host__ __device__ uint64_t operator()(uint32_t c) const { return (uint64_t)c * c; }
 };
@@ -923,27 +1031,58 @@ int sw_align_batch_device(int device, const uint8_t *d_arena, uint64_t arena_byt
 
 int sw_partition_pairs(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards, int32_t *shard,
                        uint64_t *load) {
+  // the plan sw_align_shard makes on the device (sw_shard.cuh), on the host:
+  // stable order by cells descending, snake deal over the shards
   if (n_shards < 1) return fail(SW_EINVAL, "n_shards < 1");
   if (n_pairs && (!pairs || !shard)) return fail(SW_EINVAL, "NULL pairs/shard");
-  std::vector<uint64_t> order(n_pairs);
-  std::iota(order.begin(), order.end(), 0ull);
-  auto cells = [&](uint64_t k) { return (uint64_t)pairs[k].a_len * pairs[k].b_len; };
+  std::vector<uint32_t> order(n_pairs);
+  std::iota(order.begin(), order.end(), 0u);
+  auto cells = [&](uint64_t k) {
+    return (uint64_t)std::min(pairs[k].a_len, 65535u) * std::min(pairs[k].b_len, 65535u);
+  };
   std::stable_sort(order.begin(), order.end(),
-                   [&](uint64_t x, uint64_t y) { return cells(x) > cells(y); });
-  typedef std::pair<uint64_t, int> Slot;  // (load, shard)
-  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+                   [&](uint32_t x, uint32_t y) { return cells(x) > cells(y); });
   std::vector<uint64_t> ld(n_shards, 0);
-  for (int s = 0; s < n_shards; ++s) heap.push(Slot(0, s));
-  for (uint64_t k : order) {
-    Slot t = heap.top();
-    heap.pop();
-    shard[k] = t.second;
-    t.first += cells(k);
-    ld[t.second] = t.first;
-    heap.push(t);
+  for (uint64_t p = 0; p < n_pairs; ++p) {
+    const uint64_t r = p / n_shards, q = p % n_shards;
+    const int sh = (int)((r % 2 == 0) ? q : n_shards - 1 - q);
+    shard[order[p]] = sh;
+    ld[sh] += cells(order[p]);
   }
   if (load)
     for (int s = 0; s < n_shards; ++s) load[s] = ld[s];
+  return SW_OK;
+}
+
+uint64_t sw_shard_count(uint64_t n_pairs, int n_shards, int shard) {
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return 0;
+  return shard_count(n_pairs, n_shards, shard);
+}
+
+int sw_align_shard(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
+                   uint64_t n_pairs, int shard, int n_shards, const sw_params_t *params,
+                   sw_result_t *d_out, uint32_t *d_index, void *stream, sw_timing_t *timing) {
+  const double t0 = now_ms();
+  int rc = check_params(params);
+  if (rc) return rc;
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(SW_EINVAL, "bad shard / n_shards");
+  if (n_pairs && (!arena || !pairs || !d_out || !d_index)) return fail(SW_EINVAL, "NULL buffer");
+  DeviceCtx *c = nullptr;
+  rc = get_ctx(device, &c);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(c->mu);
+  CU(cudaSetDevice(device));
+  if (timing) memset(timing, 0, sizeof(*timing));
+  if (n_pairs == 0) return SW_OK;
+  DeviceView av;
+  rc = av.init(arena, arena_bytes);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  rc = shard_run(c, av.ptr, arena_bytes, pairs, n_pairs, shard, n_shards, params, d_out, d_index, s,
+                 timing);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(s));
+  if (timing) timing->total_ms = now_ms() - t0;
   return SW_OK;
 }
 
@@ -957,60 +1096,72 @@ int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena
   if (n_devices == 1)
     return align_host(devices[0], arena, arena_bytes, pairs, n_pairs, params, out,
                       per_device_timing);
-  std::vector<int32_t> shard(n_pairs);
-  rc = sw_partition_pairs(pairs, n_pairs, n_devices, shard.data(), nullptr);
-  if (rc) return rc;
-  // per-shard deduplicated arenas + pair tables
-  struct Shard {
-    std::vector<uint8_t> arena;
-    std::vector<sw_pair_t> pairs;
-    std::vector<uint64_t> idx;
-    std::vector<sw_result_t> out;
+  if (n_pairs && (!arena || !pairs || !out)) return fail(SW_EINVAL, "NULL buffer");
+  // every device reads the caller's arena directly (pinned: zero-copy over
+  // PCIe, only its shard's bytes); pageable memory is registered once here
+  DeviceView av;
+  {
+    std::vector<DeviceCtx *> ctxs(n_devices);
+    for (int d = 0; d < n_devices; ++d) {
+      rc = get_ctx(devices[d], &ctxs[d]);
+      if (rc) return rc;
+    }
+    CU(cudaSetDevice(devices[0]));
+    rc = av.init(arena, arena_bytes);
+    if (rc) return rc;
+  }
+  struct Lane {
     int rc = 0;
     std::string err;
   };
-  std::vector<Shard> sh(n_devices);
-  std::vector<std::unordered_map<uint64_t, uint64_t>> seen(n_devices);
-  auto place = [&](Shard &S, std::unordered_map<uint64_t, uint64_t> &m, uint64_t off,
-                   uint32_t len) -> uint64_t {
-    const uint64_t key = off * 131071ull ^ len;
-    auto it = m.find(key);
-    if (it != m.end()) return it->second;
-    const uint64_t at = (S.arena.size() + 15) & ~15ull;
-    S.arena.resize(at + len);
-    if (len) memcpy(S.arena.data() + at, arena + off, len);
-    m.emplace(key, at);
-    return at;
-  };
-  for (uint64_t k = 0; k < n_pairs; ++k) {
-    const sw_pair_t &p = pairs[k];
-    if (p.a_off > arena_bytes || p.a_len > arena_bytes - p.a_off || p.b_off > arena_bytes ||
-        p.b_len > arena_bytes - p.b_off)
-      return fail(SW_EINVAL, "pair references bytes outside the arena");   // before any read
-    Shard &S = sh[shard[k]];
-    sw_pair_t q = p;
-    q.a_off = place(S, seen[shard[k]], p.a_off, p.a_len);
-    q.b_off = place(S, seen[shard[k]], p.b_off, p.b_len);
-    S.pairs.push_back(q);
-    S.idx.push_back(k);
-  }
+  std::vector<Lane> lanes(n_devices);
   std::vector<std::thread> th;
   for (int d = 0; d < n_devices; ++d) {
     th.emplace_back([&, d]() {
-      Shard &S = sh[d];
-      S.out.resize(S.pairs.size());
-      if (S.arena.empty()) S.arena.resize(16);
+      const double t0 = now_ms();
+      DeviceCtx *c = nullptr;
+      Lane &L = lanes[d];
       sw_timing_t *tm = per_device_timing ? per_device_timing + d : nullptr;
-      S.rc = align_host(devices[d], S.arena.data(), S.arena.size(), S.pairs.data(),
-                        S.pairs.size(), params, S.out.data(), tm);
-      if (S.rc) S.err = g_err;
+      if (tm) memset(tm, 0, sizeof(*tm));
+      auto body = [&]() -> int {
+        int r = get_ctx(devices[d], &c);
+        if (r) return r;
+        std::lock_guard<std::mutex> g(c->mu);
+        CU(cudaSetDevice(devices[d]));
+        const uint64_t nl = shard_count(n_pairs, n_devices, d);
+        if (nl == 0) return SW_OK;
+        CU(c->sh_out.ensure(nl * (sizeof(sw_result_t) + sizeof(uint32_t))));
+        sw_result_t *lout = (sw_result_t *)c->sh_out.p;
+        uint32_t *lidx = (uint32_t *)(lout + nl);
+        cudaStream_t s = c->stream;
+        r = shard_run(c, av.ptr, arena_bytes, pairs, n_pairs, d, n_devices, params, lout, lidx, s, tm);
+        if (r) return r;
+        // results back in input order: the shard's records and indices come
+        // down, the host scatters them into the caller's buffer
+        std::vector<sw_result_t> hout(nl);
+        std::vector<uint32_t> hidx(nl);
+        CU(cudaEventRecord(c->ev[10], s));
+        CU(cudaMemcpyAsync(hout.data(), lout, nl * sizeof(sw_result_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hidx.data(), lidx, nl * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaEventRecord(c->ev[11], s));
+        CU(cudaStreamSynchronize(s));
+        for (uint64_t r2 = 0; r2 < nl; ++r2) out[hidx[r2]] = hout[r2];
+        if (tm) {
+          tm->d2h_ms = ev_ms(c->ev[10], c->ev[11]);
+          tm->h2d_bytes = n_pairs * sizeof(sw_pair_t);
+          tm->d2h_bytes = nl * (sizeof(sw_result_t) + sizeof(uint32_t));
+        }
+        return SW_OK;
+      };
+      L.rc = body();
+      if (L.rc) L.err = g_err;
+      if (tm) tm->total_ms = now_ms() - t0;
     });
   }
   for (auto &t : th) t.join();
   for (int d = 0; d < n_devices; ++d)
-    if (sh[d].rc) return fail(sh[d].rc, "device " + std::to_string(devices[d]) + ": " + sh[d].err);
-  for (int d = 0; d < n_devices; ++d)
-    for (size_t q = 0; q < sh[d].idx.size(); ++q) out[sh[d].idx[q]] = sh[d].out[q];
+    if (lanes[d].rc)
+      return fail(lanes[d].rc, "device " + std::to_string(devices[d]) + ": " + lanes[d].err);
   return SW_OK;
 }
 
@@ -1043,7 +1194,8 @@ void sw_release(int device) {
     for (DevBuf *b : {&c->arena, &c->codes, &c->pairs, &c->out, &c->st, &c->lists, &c->ctrs,
                       &c->stats, &c->bnd, &c->pool, &c->skeys, &c->svals, &c->cubtmp,
                       &c->km_arena, &c->km_off, &c->km_len, &c->km_base, &c->km_keys, &c->km_runs,
-                      &c->km_pairs, &c->km_out, &c->km_small, &c->cta_rows})
+                      &c->km_pairs, &c->km_out, &c->km_small, &c->cta_rows, &c->sh_pairs, &c->sh_keys,
+                      &c->sh_lpairs, &c->sh_lidx, &c->sh_llen, &c->sh_loff, &c->sh_arena, &c->sh_out})
       b->release();
     c->pool_want = 0;
   }

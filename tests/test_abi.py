@@ -44,7 +44,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(_native.SwParams) == 8 + 625 * 4
 
 
-def test_partition_is_cell_balanced_lpt():
+def test_partition_is_cell_balanced_snake():
     rng = np.random.default_rng(0)
     la = rng.integers(30, 2000, 5000)
     lb = rng.integers(30, 2000, 5000)
@@ -61,6 +61,14 @@ def test_partition_is_cell_balanced_lpt():
         assert got.max() <= cells.sum() / world + cells.max()
         if world > 1:
             assert (got.max() - got.mean()) / got.mean() < 0.01
+        # the rule (sw_shard.cuh): stable descending cells, snake deal
+        order = np.argsort(-cells, kind="stable")
+        r, q = np.arange(len(order)) // world, np.arange(len(order)) % world
+        expect = np.empty(len(order), np.int32)
+        expect[order] = np.where(r % 2 == 0, q, world - 1 - q)
+        assert (shard == expect).all()
+        for s_ in range(world):
+            assert _native.shard_count(len(t), world, s_) == int((shard == s_).sum())
 
 
 def test_no_cpu_fallback_without_gpu():
