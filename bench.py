@@ -373,13 +373,13 @@ def main():
     arena_np, table_np = make_batch(args.workload, args.pairs * world, 2303, alloc=alloc)
     cells_all = int(np.dot(table_np["a_len"].astype(np.int64), table_np["b_len"].astype(np.int64)))
     n_all = len(table_np)
-    n_local = _native.shard_count(n_all, world, rank)
+    bounds = _native.shard_ranges(table_np, world)
+    n_local = int(bounds[rank + 1] - bounds[rank])
 
     # device-resident inputs for `value`
     d_arena = torch.from_numpy(arena_np).to(dev)
     d_pairs = torch.from_numpy(table_np.view(np.uint8).copy()).to(dev)
-    d_out = torch.empty(max(n_local, 1) * 32, dtype=torch.uint8, device=dev)
-    d_idx = torch.empty(max(n_local, 1), dtype=torch.int32, device=dev)
+    d_out = torch.empty((max(n_local, n_all if world == 1 else 1), 8), dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
@@ -394,22 +394,19 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return t.cpu().tolist()
 
-    def gather_to_rank0(d_rec, d_ix):
-        from paper_2303_01845_b200.distributed import gather_rows
-        rows = torch.empty((n_local, 9), dtype=torch.int32, device=dev)
-        rows[:, :8] = d_rec.view(torch.int32)[: n_local * 8].view(n_local, 8)
-        rows[:, 8] = d_ix[:n_local]
-        return gather_rows(rows, n_all, rank, world, dst=0)
+    def gather_to_rank0():
+        from paper_2303_01845_b200.distributed import gather_ranges
+        return gather_ranges(d_out[:n_local], rank, world, dst=0)
 
     def device_step():
         if world == 1:
             return _native.align_device(d_arena.data_ptr(), arena_np.size, d_pairs.data_ptr(),
                                         n_all, params, d_out.data_ptr(), device=local,
-                                        stream=stream.cuda_stream), None
-        tm = _native.align_shard(d_arena.data_ptr(), arena_np.size, d_pairs.data_ptr(), n_all,
-                                 rank, world, params, d_out.data_ptr(), d_idx.data_ptr(),
-                                 device=local, stream=stream.cuda_stream)
-        return tm, gather_to_rank0(d_out, d_idx)
+                                        stream=stream.cuda_stream), d_out
+        tm, _ = _native.align_shard(d_arena.data_ptr(), arena_np.size, d_pairs.data_ptr(), n_all,
+                                    rank, world, params, d_out.data_ptr(), device=local,
+                                    stream=stream.cuda_stream)
+        return tm, gather_to_rank0()      # records stay on rank 0's GPU
 
     step_ms, launches = [], 0
     tms = []
@@ -442,7 +439,8 @@ def main():
     dev_ms = float(np.sum(max_over_ranks(step_ms)))
     total_cells = cells_all * args.steps
     value = total_cells / (dev_ms / 1e3) / 1e9
-    rec_dev = (d_out.cpu().numpy().view(_native.RESULT_DTYPE)[:n_all] if world == 1 else gathered)
+    rec_dev = (gathered.cpu().numpy().view(_native.RESULT_DTYPE).reshape(-1)[:n_all]
+               if gathered is not None else None)
 
     # end to end through the host C-ABI call with pinned buffers
     po_ptr, po = pinned(n_all * 32)
@@ -460,9 +458,13 @@ def main():
             res = host_out
         else:
             _native.align_shard(arena_np.ctypes.data, arena_np.size, host_pairs.ctypes.data, n_all,
-                                rank, world, params, d_out.data_ptr(), d_idx.data_ptr(),
-                                device=local, stream=stream.cuda_stream)
-            res = gather_to_rank0(d_out, d_idx)      # records land on rank 0's host
+                                rank, world, params, d_out.data_ptr(), device=local,
+                                stream=stream.cuda_stream)
+            g = gather_to_rank0()               # records land on rank 0 ...
+            res = None
+            if g is not None:                   # ... and come down to its host
+                res = host_out
+                res.view(np.int32).reshape(-1, 8)[:] = g.cpu().numpy()
         return (time.perf_counter() - t0) * 1e3, res
 
     for _ in range(max(1, args.warmup)):
@@ -549,9 +551,9 @@ def main():
                    "l2": "flushed between timed steps (256 MiB memset, outside the events)",
                    "parallelism": (f"one process per GPU x{world}, weak scaling: a global batch "
                                    f"of {world} x {args.pairs} pairs held by every rank; "
-                                   "device-planned cell-balanced snake partition "
+                                   "cell-balanced contiguous ranges planned on the device "
                                    "(sw_align_shard), NCCL gather of the result records to "
-                                   "rank 0, all inside the timed region")
+                                   "rank 0's GPU, all inside the timed region")
                    if world > 1 else "1 GPU"},
         "roofline": {"bound": "int-issue", "kernel": dominant,
                      "achieved": fwd_gcups, "peak": peak_gcups, "unit": "GCUPS",
@@ -567,14 +569,14 @@ def main():
                      **cc,
                      **ncu_fields(args.workload, dev_ms / args.steps)},
         "e2e": {"value": e2e_value, "unit": "GCUPS",
-                "h2d_bytes_per_step": int(arena_np.size + table_np.nbytes) if world == 1 else
-                int(table_np.nbytes * world + arena_np.size),
+                "h2d_bytes_per_step": int(arena_np.size + table_np.nbytes),
                 "d2h_bytes_per_step": int(n_all * 32),
                 "ms_per_step": e2e_total / args.steps,
                 "alignments_per_sec": n_all * args.steps / (e2e_total / 1e3),
                 "entry": "sw_align_batch (C ABI, pinned host buffers)" if world == 1 else
-                "sw_align_shard per rank (pinned host arena read zero-copy, only the shard's "
-                "bytes) + NCCL gather of the records to rank 0 + D2H there"},
+                "sw_align_shard per rank (host plan; the range's pairs and bytes uploaded from "
+                "pinned host memory, overlapped with the forward) + NCCL gather of the records "
+                "to rank 0 + D2H there"},
         "gpu_launches": int(launches),
         "clocks": csum,
     }

@@ -128,40 +128,43 @@ int sw_align_batch_device(int device, const uint8_t *d_arena, uint64_t arena_byt
                           const sw_params_t *params, sw_result_t *d_out, void *stream,
                           sw_timing_t *timing);
 
-/* Shard a HOST batch over n_devices GPUs by cell count and gather the
- * results into `out` in input order (replaces AlignEngine's process lanes,
+/* Shard a HOST batch over n_devices GPUs by cell count and return the
+ * results in `out` in input order (replaces AlignEngine's process lanes,
  * align.py:299-335, whose _chunk split align.py:265-269 ignores lengths).
- * Every GPU plans the same partition on the device (sw_align_shard), reads
- * ONLY its shard's sequence bytes straight from the host arena (pinned
- * memory: zero-copy over PCIe; pageable memory is registered for the call)
- * and aligns them; one host thread per GPU.  per_device_timing may be NULL
- * or point to n_devices entries. */
+ * The plan (sw_shard_ranges) cuts the batch into contiguous ranges of equal
+ * cells; every GPU uploads only its range's pairs and the arena bytes they
+ * reference, overlapped with its forward pass, and writes its results
+ * straight into its part of `out`; one host thread per GPU.
+ * per_device_timing may be NULL or point to n_devices entries. */
 int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena,
                          uint64_t arena_bytes, const sw_pair_t *pairs, uint64_t n_pairs,
                          const sw_params_t *params, sw_result_t *out,
                          sw_timing_t *per_device_timing);
 
-/* One shard of a cell-balanced partition, planned on `device` (the unit of
- * the multi-process driver: one process per GPU, each calling this with its
- * rank, then gathering the records over NCCL).  The plan: pairs in stable
- * descending a_len*b_len order, dealt to the shards in a snake (sorted
- * position r*n_shards + q goes to shard q in even rounds, n_shards-1-q in odd
- * ones), so every shard's cells are within one pair of every other's.
- * `arena` and `pairs` may be device memory or host memory (pinned host
- * memory is read zero-copy); d_out / d_index are DEVICE buffers of
- * sw_shard_count(n_pairs, n_shards, shard) entries receiving the shard's
- * results and their input positions. */
+/* The cell-balanced plan: bounds[0..n_shards] with bounds[0] = 0,
+ * bounds[n_shards] = n_pairs and bounds[s] = the smallest k such that
+ * n_shards * cells(pairs[0, k)) >= s * cells(all pairs), cells = a_len*b_len:
+ * shard s takes the contiguous range [bounds[s], bounds[s+1]), and every
+ * shard's cells are within one pair's of the mean.  `pairs` may be host or
+ * device memory (then the plan runs on that device: scan + binary search). */
+int sw_shard_ranges(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards, uint64_t *bounds);
+
+/* One shard of that plan on `device` (the unit of the multi-process driver:
+ * one process per GPU, each calling this with its rank, then gathering the
+ * records over NCCL).  `arena` and `pairs` are both device memory (the plan
+ * runs on the device, only the arena bytes the range references are encoded,
+ * nothing is copied) or both host memory (the plan runs on the host; the
+ * range's pairs and the bytes they reference are uploaded, overlapped with
+ * the forward pass).  d_out is a DEVICE buffer receiving the results of
+ * pairs range[0] .. range[1]-1, in order; range (2 entries) may be NULL. */
 int sw_align_shard(int device, const uint8_t *arena, uint64_t arena_bytes,
                    const sw_pair_t *pairs, uint64_t n_pairs, int shard, int n_shards,
-                   const sw_params_t *params, sw_result_t *d_out, uint32_t *d_index,
+                   const sw_params_t *params, sw_result_t *d_out, uint64_t *range,
                    void *stream, sw_timing_t *timing);
 
-/* Pairs shard `shard` of `n_shards` receives from a batch of n_pairs. */
-uint64_t sw_shard_count(uint64_t n_pairs, int n_shards, int shard);
-
-/* The same partition computed on the host (for host drivers and tests):
- * shard[k] in [0, n_shards) for every pair; load[s] (may be NULL) receives
- * the cell total of shard s. */
+/* The same plan as a per-pair shard id, for host drivers and tests:
+ * shard[k] in [0, n_shards); load[s] (may be NULL) receives the cell total
+ * of shard s. */
 int sw_partition_pairs(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards,
                        int32_t *shard, uint64_t *load);
 

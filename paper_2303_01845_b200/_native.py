@@ -44,7 +44,7 @@ EXPORTED_SYMBOLS = (
     "sw_align_batch_multi",
     "sw_partition_pairs",
     "sw_align_shard",
-    "sw_shard_count",
+    "sw_shard_ranges",
     "sw_release",
     "sw_host_alloc",
     "sw_host_free",
@@ -147,8 +147,8 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
         lib.sw_align_shard.restype = i32
         lib.sw_align_shard.argtypes = [i32, vp, u64, vp, u64, i32, i32, ctypes.POINTER(SwParams),
                                        vp, vp, vp, ctypes.POINTER(SwTiming)]
-        lib.sw_shard_count.restype = u64
-        lib.sw_shard_count.argtypes = [u64, i32, i32]
+        lib.sw_shard_ranges.restype = i32
+        lib.sw_shard_ranges.argtypes = [vp, u64, i32, vp]
         lib.sw_partition_pairs.restype = i32
         lib.sw_partition_pairs.argtypes = [vp, u64, i32, vp, vp]
         lib.sw_release.restype = None
@@ -233,25 +233,35 @@ def align_device(d_arena: int, arena_bytes: int, d_pairs: int, n_pairs: int, par
     return tm.as_dict()
 
 
-def shard_count(n_pairs: int, n_shards: int, shard: int) -> int:
-    return int(load().sw_shard_count(n_pairs, n_shards, shard))
+def shard_ranges(pairs, n_shards: int, n_pairs: Optional[int] = None) -> np.ndarray:
+    """sw_shard_ranges: bounds[0..n_shards] of the cell-balanced contiguous
+    plan.  `pairs`: a PAIR_DTYPE array, or a device pointer with n_pairs."""
+    b = np.zeros(n_shards + 1, dtype=np.uint64)
+    if isinstance(pairs, np.ndarray):
+        pairs = np.ascontiguousarray(pairs, dtype=PAIR_DTYPE)
+        ptr, n = _ptr(pairs), len(pairs)
+    else:
+        ptr, n = int(pairs), int(n_pairs)
+    _check(load().sw_shard_ranges(ptr, n, n_shards, b.ctypes.data))
+    return b
 
 
 def align_shard(arena_ptr: int, arena_bytes: int, pairs_ptr: int, n_pairs: int, shard: int,
-                n_shards: int, params: SwParams, d_out: int, d_index: int, device: int = 0,
-                stream: int = 0) -> dict:
-    """sw_align_shard: shard `shard` of a batch (arena / pairs: device or host
-    pointers) into the DEVICE buffers d_out (results) and d_index (uint32
-    input positions)."""
+                n_shards: int, params: SwParams, d_out: int, device: int = 0,
+                stream: int = 0):
+    """sw_align_shard: shard `shard` of a batch (arena and pairs both device or
+    both host pointers) into the DEVICE buffer d_out.  Returns (timing dict,
+    (first, end)) -- d_out holds the results of pairs first .. end-1."""
     tm = SwTiming()
+    rng = np.zeros(2, dtype=np.uint64)
     _check(load().sw_align_shard(device, arena_ptr, arena_bytes, pairs_ptr, n_pairs, shard,
-                                 n_shards, ctypes.byref(params), d_out, d_index, stream or None,
-                                 ctypes.byref(tm)))
-    return tm.as_dict()
+                                 n_shards, ctypes.byref(params), d_out, rng.ctypes.data,
+                                 stream or None, ctypes.byref(tm)))
+    return tm.as_dict(), (int(rng[0]), int(rng[1]))
 
 
 def partition(pairs: np.ndarray, n_shards: int):
-    """sw_partition_pairs: the cell-balanced snake partition, on the host."""
+    """sw_partition_pairs: the cell-balanced plan as a shard id per pair."""
     lib = load()
     pairs = np.ascontiguousarray(pairs, dtype=PAIR_DTYPE)
     shard = np.empty(len(pairs), dtype=np.int32)

@@ -257,7 +257,9 @@ except ImportError:  # pragma: no cover
             self.kernel_seconds += other.kernel_seconds
 
 
-def _align(pairs: Sequence[tuple], params: AlignParams, devices) -> tuple:
+def _align(pairs: Sequence[tuple], params: AlignParams, devices, gpu_lock=None) -> tuple:
+    """pack (host, C threads) -> align (GPU; under gpu_lock when given, so a
+    second in-flight batch packs while this one runs) -> lazy results."""
     t0 = perf_counter()
     pool = _native.pinned_pool()
     bufs = []
@@ -270,7 +272,12 @@ def _align(pairs: Sequence[tuple], params: AlignParams, devices) -> tuple:
     try:
         batch = pack_pairs(pairs, alloc=alloc)
         t1 = perf_counter()
-        rec, timings = align_packed(batch, params, devices)
+        if gpu_lock is None:
+            rec, timings = align_packed(batch, params, devices)
+        else:
+            with gpu_lock:
+                t1 = perf_counter()
+                rec, timings = align_packed(batch, params, devices)
     finally:
         for b in bufs:
             b.release()
@@ -312,7 +319,10 @@ class AlignEngine:
     `lanes` = number of GPUs a batch is sharded over (cell-balanced, capped at
     the visible device count).  With use_processes=True, submit() returns
     immediately and the batch runs on a host thread (the reference's async
-    pool semantics, needed by pre-blocking, pipeline.py:209-212)."""
+    pool semantics, needed by pre-blocking, pipeline.py:209-212); two host
+    threads, so the next batch's packing overlaps this batch's GPU work (the
+    GPU phase is serialised by a lock; results come back per batch, in order
+    of each handle's result())."""
 
     def __init__(self, params: AlignParams, lanes: int = 1, use_processes: bool = False):
         if lanes < 1:
@@ -329,14 +339,13 @@ class AlignEngine:
         if self._devices is None:
             self._devices = _device_ids(self.lanes)
         if self.use_processes and self._pool is None:
-            self._pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="pastis-gpu")
+            self._pool = ThreadPoolExecutor(max_workers=2, thread_name_prefix="pastis-gpu")
 
     def _run(self, pairs: list) -> tuple:
         t0 = perf_counter()
-        with self._lock:
-            results, errors, counters, timings, phases = _align(pairs, self.params,
-                                                                self._devices)
-            self.last_phases = phases
+        results, errors, counters, timings, phases = _align(pairs, self.params, self._devices,
+                                                            gpu_lock=self._lock)
+        self.last_phases = phases
         wall = perf_counter() - t0
         if len(timings) <= 1:
             lanes = [(self._devices[0], counters.kernel_seconds, wall)]

@@ -34,7 +34,6 @@
 #include "sw_cta_packed.cuh"
 #include "sw_fasta.h"
 #include "sw_kmer.cuh"
-#include "sw_shard.cuh"
 
 using namespace pastis;
 
@@ -92,7 +91,7 @@ struct DeviceCtx {
   DevBuf arena, codes, pairs, out, st, lists, ctrs, stats, mat, lut, bnd, pool;
   // sharding (sw_align_shard / sw_align_batch_multi): the whole pair table,
   // sort keys, the shard's pair table / indices / lengths / offsets, its arena
-  DevBuf sh_pairs, sh_keys, sh_lpairs, sh_lidx, sh_llen, sh_loff, sh_arena, sh_out;
+  DevBuf sh_cells;
   DevBuf skeys, svals, cubtmp;  // work-list sort
   DevBuf km_arena, km_off, km_len, km_base, km_keys, km_runs, km_pairs, km_out, km_small;
   cudaEvent_t ev[16];
@@ -299,11 +298,13 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // `ready`/`slice_bytes`/`arena_done`: host-pipelined arena (align_host) --
 // the packed forward waits per pair for its slices, everything reading the
 // encoded arena waits for arena_done; nullptr = the arena is resident.
+// `arena_lo`: only arena offsets [arena_lo, arena_bytes) are present;
+// d_arena is the virtual base (d_arena + off is valid in that range).
 int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
                const sw_pair_t *d_pairs, uint64_t n_pairs, const sw_params_t *prm,
                sw_result_t *d_out, cudaStream_t s, sw_timing_t *tm,
                const uint32_t *ready = nullptr, uint64_t slice_bytes = 0,
-               cudaEvent_t arena_done = nullptr) {
+               cudaEvent_t arena_done = nullptr, uint64_t arena_lo = 0) {
   if (n_pairs == 0) return SW_OK;
   if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
   // the chain runs on the greatest-priority stream, joined back to `s` at the end
@@ -316,7 +317,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   uint32_t launches = 0;
   const double h0 = now_ms();
   // device buffers
-  CU(c->codes.ensure(arena_bytes + 64));
+  CU(c->codes.ensure(arena_bytes - arena_lo + 64));
   CU(c->st.ensure(n_pairs * sizeof(PairState)));
   CU(c->lists.ensure((size_t)kStages * kNumClasses * n_pairs * 4));
   CU(c->ctrs.ensure(2 * kStages * kNumClasses * 4));
@@ -336,9 +337,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   memset(&A, 0, sizeof(A));
   // codes[i] = lut[raw[i]] at the raw arena's address modulo 16, so k_encode
   // moves aligned 128-bit words whatever the caller's pointer alignment
-  uint8_t *codes = (uint8_t *)c->codes.p + ((uintptr_t)d_arena & 15u);
+  uint8_t *codes_lo = (uint8_t *)c->codes.p + ((uintptr_t)(d_arena + arena_lo) & 15u);
+  uint8_t *codes = codes_lo - arena_lo;       // virtual base, like d_arena
   A.codes = codes;
   A.raw = d_arena;
+  A.arena_lo = arena_lo;
   A.pairs = d_pairs;
   A.st = (PairState *)c->st.p;
   A.out = d_out;
@@ -376,8 +379,9 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   CU(cudaEventRecord(c->ev[0], s));
   if (!arena_done) {   // resident arena: encode first, every kernel reads codes
     const int threads = 256;
-    uint64_t blocks = std::min<uint64_t>((arena_bytes / 16 + threads) / threads + 1, (uint64_t)c->sms * 8);
-    k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, codes, arena_bytes,
+    uint64_t blocks = std::min<uint64_t>(((arena_bytes - arena_lo) / 16 + threads) / threads + 1,
+                                         (uint64_t)c->sms * 8);
+    k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena + arena_lo, codes_lo, arena_bytes - arena_lo,
                                                  (const uint8_t *)c->lut.p);
     ++launches;
   }
@@ -477,9 +481,10 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
       // has landed
       CU(cudaStreamWaitEvent(s, arena_done, 0));
       const int threads = 256;
-      uint64_t blocks = std::min<uint64_t>((arena_bytes / 16 + threads) / threads + 1, (uint64_t)c->sms * 8);
-      k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena, codes, arena_bytes,
-                                                   (const uint8_t *)c->lut.p);
+      uint64_t blocks = std::min<uint64_t>(((arena_bytes - arena_lo) / 16 + threads) / threads + 1,
+                                           (uint64_t)c->sms * 8);
+      k_encode<<<(unsigned)blocks, threads, 0, s>>>(d_arena + arena_lo, codes_lo,
+                                                   arena_bytes - arena_lo, (const uint8_t *)c->lut.p);
       ++launches;
     }
     // long pairs: scalar forward concurrently with the packed classes -- one
@@ -626,102 +631,95 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   return SW_OK;
 }
 
-int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
-               uint64_t n_pairs, const sw_params_t *params, sw_result_t *out, sw_timing_t *tm) {
+// Pairs [k0, k1) of a HOST batch on `device`: the range's pair table and the
+// arena bytes it references ([lo, hi), the whole arena for a whole batch)
+// are uploaded on the copy stream -- the table first (the planning kernels
+// need it), then the bytes in slices, each followed by a 4-byte copy that
+// bumps `ready`; the packed forward starts as soon as its pairs' slices have
+// landed, so the upload overlaps the forward pass.  Results go to `out`
+// (pairs k0.. in order): host memory, or device memory when out_on_device.
+int align_range(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
+                uint64_t k0, uint64_t k1, bool whole, const sw_params_t *params, sw_result_t *out,
+                bool out_on_device, cudaStream_t user_stream, sw_timing_t *tm) {
   const double t0 = now_ms();
-  int rc = check_params(params);
-  if (rc) return rc;
-  if (n_pairs && (!pairs || !out)) return fail(SW_EINVAL, "NULL pairs/out");
-  // pair bounds are checked on the device by k_classify (no host pass over the table)
-  const double t_valid = now_ms();
+  const uint64_t n_pairs = k1 - k0;
   DeviceCtx *c = nullptr;
-  rc = get_ctx(device, &c);
+  int rc = get_ctx(device, &c);
   if (rc) return rc;
   std::lock_guard<std::mutex> g(c->mu);
   CU(cudaSetDevice(device));
   const double t_ctx = now_ms();
   if (tm) memset(tm, 0, sizeof(*tm));
   if (n_pairs == 0) return SW_OK;
-  cudaStream_t s = c->stream;
-  CU(c->arena.ensure(arena_bytes + 64));
+  // the byte range the pairs reference (pairs outside the arena are left to
+  // the device check: the range is clamped to the arena)
+  uint64_t lo = 0, hi = arena_bytes;
+  if (!whole) {
+    lo = ~0ull;
+    hi = 0;
+    for (uint64_t k = k0; k < k1; ++k) {
+      const sw_pair_t &p = pairs[k];
+      lo = std::min(lo, std::min(p.a_off, p.b_off));
+      hi = std::max(hi, std::max(p.a_off + p.a_len, p.b_off + p.b_len));
+    }
+    hi = std::min(hi, arena_bytes);
+    lo = std::min(lo, hi);
+  }
+  cudaStream_t s = user_stream ? user_stream : c->stream;
+  const uint64_t span = hi - lo;
+  CU(c->arena.ensure(span + 64));
   CU(c->pairs.ensure(n_pairs * sizeof(sw_pair_t)));
-  CU(c->out.ensure(n_pairs * sizeof(sw_result_t)));
-  // Upload on the copy stream: the pair table first (the planning kernels
-  // need it), then the arena in slices, each followed by a 4-byte copy that
-  // bumps `ready`; the packed forward starts as soon as its pairs' slices
-  // have landed, so the arena upload overlaps the forward pass.
+  if (!out_on_device) CU(c->out.ensure(n_pairs * sizeof(sw_result_t)));
+  sw_result_t *d_out = out_on_device ? out : (sw_result_t *)c->out.p;
   cudaStream_t cs = c->copy_stream;
-  const uint64_t slice = std::max<uint64_t>((uint64_t)4 << 20,
-                                            (arena_bytes + kMaxSlices - 1) / kMaxSlices);
-  const int nslices = (int)((arena_bytes + slice - 1) / slice);
-  const double t_ev8 = now_ms();
+  const uint64_t slice = std::max<uint64_t>((uint64_t)4 << 20, (span + kMaxSlices - 1) / kMaxSlices);
+  const int nslices = (int)((span + slice - 1) / slice);
   CU(cudaEventRecord(c->ev[8], s));
   CU(cudaStreamWaitEvent(cs, c->ev[8], 0));
   CU(cudaMemsetAsync(c->readyb.p, 0, 4, cs));
-  CU(cudaMemcpyAsync(c->pairs.p, pairs, n_pairs * sizeof(sw_pair_t), cudaMemcpyHostToDevice, cs));
+  CU(cudaMemcpyAsync(c->pairs.p, pairs + k0, n_pairs * sizeof(sw_pair_t), cudaMemcpyHostToDevice, cs));
   CU(cudaEventRecord(c->ev_pairs, cs));
   for (int k = 0; k < nslices; ++k) {
-    const uint64_t b0 = (uint64_t)k * slice, nb = std::min<uint64_t>(slice, arena_bytes - b0);
-    CU(cudaMemcpyAsync((uint8_t *)c->arena.p + b0, arena + b0, nb, cudaMemcpyHostToDevice, cs));
+    const uint64_t b0 = (uint64_t)k * slice, nb = std::min<uint64_t>(slice, span - b0);
+    CU(cudaMemcpyAsync((uint8_t *)c->arena.p + b0, arena + lo + b0, nb, cudaMemcpyHostToDevice, cs));
     CU(cudaMemcpyAsync(c->readyb.p, c->slice_vals + k, 4, cudaMemcpyHostToDevice, cs));
   }
   CU(cudaEventRecord(c->ev_arena, cs));
   CU(cudaStreamWaitEvent(s, c->ev_pairs, 0));
-  rc = run_device(c, (const uint8_t *)c->arena.p, arena_bytes, (const sw_pair_t *)c->pairs.p,
-                  n_pairs, params, (sw_result_t *)c->out.p, s, tm,
-                  nslices > 0 ? (const uint32_t *)c->readyb.p : nullptr, slice, c->ev_arena);
+  rc = run_device(c, (const uint8_t *)c->arena.p - lo, hi, (const sw_pair_t *)c->pairs.p, n_pairs,
+                  params, d_out, s, tm, nslices > 0 ? (const uint32_t *)c->readyb.p : nullptr, slice,
+                  c->ev_arena, lo);
   if (rc) return rc;
   CU(cudaEventRecord(c->ev[10], s));
-  CU(cudaMemcpyAsync(out, c->out.p, n_pairs * sizeof(sw_result_t), cudaMemcpyDeviceToHost, s));
+  if (!out_on_device)
+    CU(cudaMemcpyAsync(out, d_out, n_pairs * sizeof(sw_result_t), cudaMemcpyDeviceToHost, s));
   CU(cudaEventRecord(c->ev[11], s));
   const double t_issued = now_ms();
   CU(cudaStreamSynchronize(s));
   if (getenv("PASTIS_SW_DEBUG_E2E")) {
-    fprintf(stderr, "e2e: valid=%.3f ctx=%.3f ev8=%.3f ", t_valid - t0, t_ctx - t0, t_ev8 - t0);
-    fprintf(stderr, "e2e: host_issue=%.3f pre_kernel(ev8->ev0)=%.3f kernel(ev0->ev10)=%.3f d2h=%.3f wall=%.3f\n",
-            t_issued - t0, ev_ms(c->ev[8], c->ev[0]), ev_ms(c->ev[0], c->ev[10]),
-            ev_ms(c->ev[10], c->ev[11]), now_ms() - t0);
+    fprintf(stderr, "e2e: ctx=%.3f host_issue=%.3f pre_kernel(ev8->ev0)=%.3f kernel(ev0->ev10)=%.3f "
+            "d2h=%.3f wall=%.3f\n", t_ctx - t0, t_issued - t0, ev_ms(c->ev[8], c->ev[0]),
+            ev_ms(c->ev[0], c->ev[10]), ev_ms(c->ev[10], c->ev[11]), now_ms() - t0);
   }
   if (tm) {
     tm->h2d_ms = ev_ms(c->ev[8], c->ev_arena);   // overlaps the forward pass
     tm->d2h_ms = ev_ms(c->ev[10], c->ev[11]);
-    tm->h2d_bytes = arena_bytes + n_pairs * sizeof(sw_pair_t);
-    tm->d2h_bytes = n_pairs * sizeof(sw_result_t);
+    tm->h2d_bytes = span + n_pairs * sizeof(sw_pair_t);
+    tm->d2h_bytes = out_on_device ? 0 : n_pairs * sizeof(sw_result_t);
     tm->total_ms = now_ms() - t0;
   }
   return SW_OK;
 }
 
-// A caller's arena as a pointer the device can read: device memory as is,
-// pinned host memory through its mapped device address; pageable host memory
-// is registered (mapped, read-only) for the duration of the call.
-struct DeviceView {
-  const uint8_t *ptr = nullptr;
-  void *registered = nullptr;
-  int init(const void *host_or_dev, uint64_t bytes) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, host_or_dev) != cudaSuccess) {
-      cudaGetLastError();
-      at.type = cudaMemoryTypeUnregistered;
-    }
-    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
-      ptr = (const uint8_t *)host_or_dev;
-      return SW_OK;
-    }
-    if (at.type == cudaMemoryTypeUnregistered) {
-      CU(cudaHostRegister(const_cast<void *>(host_or_dev), std::max<uint64_t>(bytes, 1),
-                          cudaHostRegisterPortable | cudaHostRegisterMapped | cudaHostRegisterReadOnly));
-      registered = const_cast<void *>(host_or_dev);
-    }
-    void *d = nullptr;
-    CU(cudaHostGetDevicePointer(&d, const_cast<void *>(host_or_dev), 0));
-    ptr = (const uint8_t *)d;
-    return SW_OK;
-  }
-  ~DeviceView() {
-    if (registered) cudaHostUnregister(registered);
-  }
-};
+int align_host(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
+               uint64_t n_pairs, const sw_params_t *params, sw_result_t *out, sw_timing_t *tm) {
+  int rc = check_params(params);
+  if (rc) return rc;
+  if (n_pairs && (!pairs || !out)) return fail(SW_EINVAL, "NULL pairs/out");
+  // pair bounds are checked on the device by k_classify (no host pass over the table)
+  return align_range(device, arena, arena_bytes, pairs, 0, n_pairs, true, params, out, false,
+                     nullptr, tm);
+}
 
 bool is_device_ptr(const void *p) {
   cudaPointerAttributes at;
@@ -732,67 +730,117 @@ bool is_device_ptr(const void *p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-// Shard `shard` of `n_shards` of a batch on device c (caller holds c->mu and
-// has set the device): plan on the device (sw_shard.cuh), gather the shard's
-// sequences from `arena` (device-readable: device memory or mapped pinned
-// host memory), align them.  Writes the shard's results to d_lout and their
-// input indices to d_lidx (shard_count entries each).
-int shard_run(DeviceCtx *c, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
-              uint64_t n_pairs, int shard, int n_shards, const sw_params_t *prm,
-              sw_result_t *d_lout, uint32_t *d_lidx, cudaStream_t s, sw_timing_t *tm) {
-  if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
-  const uint64_t nl = shard_count(n_pairs, n_shards, shard);
-  if (nl == 0) return SW_OK;
-  uint32_t launches = 0;
-  // the whole table on the device (the plan needs every pair's cells)
-  const sw_pair_t *d_pairs = pairs;
-  if (!is_device_ptr(pairs)) {
-    CU(c->sh_pairs.ensure(n_pairs * sizeof(sw_pair_t)));
-    CU(cudaMemcpyAsync(c->sh_pairs.p, pairs, n_pairs * sizeof(sw_pair_t), cudaMemcpyHostToDevice, s));
-    d_pairs = (const sw_pair_t *)c->sh_pairs.p;
+// Cell-balanced contiguous split of a batch into N ranges (the plan of
+// sw_align_shard / sw_align_batch_multi): bounds[s] = the smallest k with
+// N * cells(pairs[0, k)) >= s * total (cells = a_len * b_len), bounds[0] = 0,
+// bounds[N] = n.  Every range's cells are within one pair's of total / N.
+// Host version: per-chunk sums, then each chunk scans for the targets that
+// fall inside it (several threads).
+void plan_ranges_host(const sw_pair_t *pairs, uint64_t n, int N, uint64_t *bounds) {
+  typedef unsigned __int128 u128;
+  bounds[0] = 0;
+  bounds[N] = n;
+  if (N == 1) return;
+  const int T = (int)std::max<uint64_t>(1, std::min<uint64_t>(16, n / 65536));
+  std::vector<u128> part(T + 1, 0);
+  auto cells = [&](uint64_t k) { return (uint64_t)pairs[k].a_len * pairs[k].b_len; };
+  auto run = [&](auto &&fn) {
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(fn, t);
+    fn(0);
+    for (auto &x : th) x.join();
+  };
+  run([&](int t) {
+    u128 acc = 0;
+    for (uint64_t k = n * t / T, e = n * (t + 1) / T; k < e; ++k) acc += cells(k);
+    part[t + 1] = acc;
+  });
+  for (int t = 0; t < T; ++t) part[t + 1] += part[t];
+  const u128 total = part[T];
+  for (int s = 1; s < N; ++s) bounds[s] = total == 0 ? 0 : n;
+  if (total == 0) return;
+  run([&](int t) {
+    u128 acc = part[t];
+    int s = 1;
+    while (s < N && (u128)s * total <= acc * (u128)N) ++s;   // targets of earlier chunks
+    for (uint64_t k = n * t / T, e = n * (t + 1) / T; k < e && s < N; ++k) {
+      acc += cells(k);
+      for (; s < N && acc * (u128)N >= (u128)s * total; ++s) bounds[s] = k + 1;
+    }
+  });
+}
+
+// The same plan on the device for a device-resident table (one sync).
+__global__ void k_range_cells(const sw_pair_t *__restrict__ pairs, uint64_t n, uint64_t *cells) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) cells[k] = (uint64_t)pairs[k].a_len * pairs[k].b_len;
+}
+__global__ void k_range_bounds(const uint64_t *__restrict__ incl, uint64_t n, int N,
+                               uint64_t *bounds) {
+  typedef unsigned __int128 u128;
+  const int s = threadIdx.x;
+  if (s > N) return;
+  if (s == 0 || s == N) { bounds[s] = s == 0 ? 0 : n; return; }
+  const u128 total = incl[n - 1];
+  if (total == 0) { bounds[s] = 0; return; }
+  // smallest k with N * prefix(k) >= s * total, prefix(k) = incl[k - 1]
+  uint64_t lo = 1, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if ((u128)incl[mid - 1] * (u128)N >= (u128)s * total) hi = mid;
+    else lo = mid + 1;
   }
-  CU(c->sh_keys.ensure(4 * n_pairs * sizeof(uint32_t)));
-  uint32_t *k_in = (uint32_t *)c->sh_keys.p, *k_out = k_in + n_pairs;
-  uint32_t *v_in = k_out + n_pairs, *v_out = v_in + n_pairs;
-  k_shard_keys<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(d_pairs, n_pairs, k_in, v_in);
-  ++launches;
+  bounds[s] = lo;
+}
+
+// byte span [lo, hi) the pairs of range `shard` reference (lo/hi preset to
+// ~0 / 0): the device path encodes only that part of the arena
+__global__ void k_range_span(const sw_pair_t *__restrict__ pairs, const uint64_t *__restrict__ bounds,
+                             int shard, unsigned long long *span) {
+  const uint64_t b = bounds[shard], e = bounds[shard + 1];
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (uint64_t k = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const sw_pair_t p = pairs[k];
+    lo = min(lo, (unsigned long long)min(p.a_off, p.b_off));
+    hi = max(hi, (unsigned long long)max(p.a_off + p.a_len, p.b_off + p.b_len));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&span[0], lo);
+    atomicMax(&span[1], hi);
+  }
+}
+
+// bounds[0..N] of the plan; with shard >= 0 also span[0..1] = the byte range
+// that shard's pairs reference
+int plan_ranges_device(DeviceCtx *c, const sw_pair_t *d_pairs, uint64_t n, int N, uint64_t *bounds,
+                       cudaStream_t s, int shard = -1, uint64_t *span = nullptr) {
+  CU(c->sh_cells.ensure(2 * n * sizeof(uint64_t) + (N + 3) * sizeof(uint64_t)));
+  uint64_t *cells = (uint64_t *)c->sh_cells.p, *incl = cells + n, *db = incl + n;
+  unsigned long long *dspan = (unsigned long long *)(db + N + 1);
+  k_range_cells<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d_pairs, n, cells);
   CU(cudaGetLastError());
   size_t tmp_bytes = 0;
-  CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out, (int)n_pairs, 0, 32, s));
+  CU(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cells, incl, (int)n, s));
   CU(c->cubtmp.ensure(tmp_bytes));
-  CU(cub::DeviceRadixSort::SortPairs(c->cubtmp.p, tmp_bytes, k_in, k_out, v_in, v_out, (int)n_pairs, 0, 32, s));
-  launches += 5;
-  CU(c->sh_lpairs.ensure(nl * sizeof(sw_pair_t)));
-  CU(c->sh_llen.ensure(nl * sizeof(uint64_t)));
-  CU(c->sh_loff.ensure(nl * sizeof(uint64_t) + 16));
-  sw_pair_t *lpairs = (sw_pair_t *)c->sh_lpairs.p;
-  uint64_t *llen = (uint64_t *)c->sh_llen.p, *loff = (uint64_t *)c->sh_loff.p;
-  k_shard_select<<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(v_out, d_pairs, n_shards, shard, nl,
-                                                             lpairs, d_lidx, llen);
-  ++launches;
+  CU(cub::DeviceScan::InclusiveSum(c->cubtmp.p, tmp_bytes, cells, incl, (int)n, s));
+  k_range_bounds<<<1, 1024, 0, s>>>(incl, n, N, db);
   CU(cudaGetLastError());
-  tmp_bytes = 0;
-  CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, llen, loff, (int)nl, s));
-  CU(c->cubtmp.ensure(tmp_bytes));
-  CU(cub::DeviceScan::ExclusiveSum(c->cubtmp.p, tmp_bytes, llen, loff, (int)nl, s));
-  launches += 2;
-  uint64_t last[2] = {0, 0};
-  CU(cudaMemcpyAsync(&last[0], loff + nl - 1, 8, cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(&last[1], llen + nl - 1, 8, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  const uint64_t local_bytes = last[0] + last[1];
-  CU(c->sh_arena.ensure(local_bytes + 64));
-  {
-    const unsigned blocks = (unsigned)std::min<uint64_t>((nl + 7) / 8, (uint64_t)c->sms * 16);
-    k_shard_gather<<<blocks, 256, 0, s>>>(arena, arena_bytes, lpairs, loff, nl,
-                                          (uint8_t *)c->sh_arena.p, local_bytes);
-    ++launches;
+  if (shard >= 0) {
+    const unsigned long long init[2] = {~0ull, 0ull};
+    CU(cudaMemcpyAsync(dspan, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    k_range_span<<<c->sms * 2, 256, 0, s>>>(d_pairs, db, shard, dspan);
     CU(cudaGetLastError());
   }
-  int rc = run_device(c, (const uint8_t *)c->sh_arena.p, std::max<uint64_t>(local_bytes, 1), lpairs,
-                      nl, prm, d_lout, s, tm);
-  if (rc) return rc;
-  if (tm) tm->launches += launches;
+  std::vector<uint64_t> h(N + 3);
+  CU(cudaMemcpyAsync(h.data(), db, (N + 3) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  for (int k = 0; k <= N; ++k) bounds[k] = h[k];
+  if (span) { span[0] = h[N + 1]; span[1] = h[N + 2]; }
   return SW_OK;
 }
 
@@ -1031,57 +1079,83 @@ int sw_align_batch_device(int device, const uint8_t *d_arena, uint64_t arena_byt
 
 int sw_partition_pairs(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards, int32_t *shard,
                        uint64_t *load) {
-  // the plan sw_align_shard makes on the device (sw_shard.cuh), on the host:
-  // stable order by cells descending, snake deal over the shards
+  // the plan of sw_align_shard / sw_align_batch_multi, per pair
   if (n_shards < 1) return fail(SW_EINVAL, "n_shards < 1");
   if (n_pairs && (!pairs || !shard)) return fail(SW_EINVAL, "NULL pairs/shard");
-  std::vector<uint32_t> order(n_pairs);
-  std::iota(order.begin(), order.end(), 0u);
-  auto cells = [&](uint64_t k) {
-    return (uint64_t)std::min(pairs[k].a_len, 65535u) * std::min(pairs[k].b_len, 65535u);
-  };
-  std::stable_sort(order.begin(), order.end(),
-                   [&](uint32_t x, uint32_t y) { return cells(x) > cells(y); });
-  std::vector<uint64_t> ld(n_shards, 0);
-  for (uint64_t p = 0; p < n_pairs; ++p) {
-    const uint64_t r = p / n_shards, q = p % n_shards;
-    const int sh = (int)((r % 2 == 0) ? q : n_shards - 1 - q);
-    shard[order[p]] = sh;
-    ld[sh] += cells(order[p]);
+  std::vector<uint64_t> b(n_shards + 1);
+  plan_ranges_host(pairs, n_pairs, n_shards, b.data());
+  for (int s = 0; s < n_shards; ++s) {
+    uint64_t ld = 0;
+    for (uint64_t k = b[s]; k < b[s + 1]; ++k) {
+      shard[k] = s;
+      ld += (uint64_t)pairs[k].a_len * pairs[k].b_len;
+    }
+    if (load) load[s] = ld;
   }
-  if (load)
-    for (int s = 0; s < n_shards; ++s) load[s] = ld[s];
   return SW_OK;
 }
 
-uint64_t sw_shard_count(uint64_t n_pairs, int n_shards, int shard) {
-  if (n_shards < 1 || shard < 0 || shard >= n_shards) return 0;
-  return shard_count(n_pairs, n_shards, shard);
+int sw_shard_ranges(const sw_pair_t *pairs, uint64_t n_pairs, int n_shards, uint64_t *bounds) {
+  if (n_shards < 1 || !bounds) return fail(SW_EINVAL, "bad n_shards / bounds");
+  if (n_pairs && !pairs) return fail(SW_EINVAL, "NULL pairs");
+  if (n_pairs && is_device_ptr(pairs)) {
+    cudaPointerAttributes at;
+    CU(cudaPointerGetAttributes(&at, pairs));
+    DeviceCtx *c = nullptr;
+    int rc = get_ctx(at.device, &c);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(at.device));
+    return plan_ranges_device(c, pairs, n_pairs, n_shards, bounds, c->stream);
+  }
+  plan_ranges_host(pairs, n_pairs, n_shards, bounds);
+  return SW_OK;
 }
 
 int sw_align_shard(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
                    uint64_t n_pairs, int shard, int n_shards, const sw_params_t *params,
-                   sw_result_t *d_out, uint32_t *d_index, void *stream, sw_timing_t *timing) {
+                   sw_result_t *d_out, uint64_t *range, void *stream, sw_timing_t *timing) {
   const double t0 = now_ms();
   int rc = check_params(params);
   if (rc) return rc;
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(SW_EINVAL, "bad shard / n_shards");
-  if (n_pairs && (!arena || !pairs || !d_out || !d_index)) return fail(SW_EINVAL, "NULL buffer");
-  DeviceCtx *c = nullptr;
-  rc = get_ctx(device, &c);
-  if (rc) return rc;
-  std::lock_guard<std::mutex> g(c->mu);
-  CU(cudaSetDevice(device));
+  if (n_pairs && (!arena || !pairs || !d_out)) return fail(SW_EINVAL, "NULL buffer");
   if (timing) memset(timing, 0, sizeof(*timing));
-  if (n_pairs == 0) return SW_OK;
-  DeviceView av;
-  rc = av.init(arena, arena_bytes);
-  if (rc) return rc;
-  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  rc = shard_run(c, av.ptr, arena_bytes, pairs, n_pairs, shard, n_shards, params, d_out, d_index, s,
-                 timing);
-  if (rc) return rc;
-  CU(cudaStreamSynchronize(s));
+  std::vector<uint64_t> b(n_shards + 1, 0);
+  const bool dev_pairs = n_pairs && is_device_ptr(pairs);
+  if (dev_pairs != (n_pairs && is_device_ptr(arena)))
+    return fail(SW_EINVAL, "arena and pairs must both be device or both be host memory");
+  if (dev_pairs) {
+    // everything resident on the device: plan there, align the range in place
+    DeviceCtx *c = nullptr;
+    rc = get_ctx(device, &c);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> g(c->mu);
+    CU(cudaSetDevice(device));
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    const double h0 = now_ms();
+    uint64_t span[2] = {0, 0};
+    rc = plan_ranges_device(c, pairs, n_pairs, n_shards, b.data(), s, shard, span);
+    if (rc) return rc;
+    if (timing) timing->host_plan_ms += now_ms() - h0;
+    if (range) { range[0] = b[shard]; range[1] = b[shard + 1]; }
+    // only the arena bytes this range references are encoded (clamped: pairs
+    // outside the arena are rejected by the planning kernel)
+    const uint64_t hi = std::min<uint64_t>(span[1], arena_bytes), lo = std::min(span[0], hi);
+    rc = run_device(c, arena, hi, pairs + b[shard], b[shard + 1] - b[shard], params, d_out, s,
+                    timing, nullptr, 0, nullptr, lo);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(s));
+  } else {
+    const double h0 = now_ms();
+    plan_ranges_host(pairs, n_pairs, n_shards, b.data());
+    const double h1 = now_ms();
+    if (range) { range[0] = b[shard]; range[1] = b[shard + 1]; }
+    rc = align_range(device, arena, arena_bytes, pairs, b[shard], b[shard + 1], false, params, d_out,
+                     true, (cudaStream_t)stream, timing);
+    if (rc) return rc;
+    if (timing) timing->host_plan_ms += h1 - h0;
+  }
   if (timing) timing->total_ms = now_ms() - t0;
   return SW_OK;
 }
@@ -1097,19 +1171,10 @@ int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena
     return align_host(devices[0], arena, arena_bytes, pairs, n_pairs, params, out,
                       per_device_timing);
   if (n_pairs && (!arena || !pairs || !out)) return fail(SW_EINVAL, "NULL buffer");
-  // every device reads the caller's arena directly (pinned: zero-copy over
-  // PCIe, only its shard's bytes); pageable memory is registered once here
-  DeviceView av;
-  {
-    std::vector<DeviceCtx *> ctxs(n_devices);
-    for (int d = 0; d < n_devices; ++d) {
-      rc = get_ctx(devices[d], &ctxs[d]);
-      if (rc) return rc;
-    }
-    CU(cudaSetDevice(devices[0]));
-    rc = av.init(arena, arena_bytes);
-    if (rc) return rc;
-  }
+  const double h0 = now_ms();
+  std::vector<uint64_t> b(n_devices + 1);
+  plan_ranges_host(pairs, n_pairs, n_devices, b.data());
+  const double plan_ms = now_ms() - h0;
   struct Lane {
     int rc = 0;
     std::string err;
@@ -1118,44 +1183,15 @@ int sw_align_batch_multi(int n_devices, const int *devices, const uint8_t *arena
   std::vector<std::thread> th;
   for (int d = 0; d < n_devices; ++d) {
     th.emplace_back([&, d]() {
-      const double t0 = now_ms();
-      DeviceCtx *c = nullptr;
-      Lane &L = lanes[d];
       sw_timing_t *tm = per_device_timing ? per_device_timing + d : nullptr;
-      if (tm) memset(tm, 0, sizeof(*tm));
-      auto body = [&]() -> int {
-        int r = get_ctx(devices[d], &c);
-        if (r) return r;
-        std::lock_guard<std::mutex> g(c->mu);
-        CU(cudaSetDevice(devices[d]));
-        const uint64_t nl = shard_count(n_pairs, n_devices, d);
-        if (nl == 0) return SW_OK;
-        CU(c->sh_out.ensure(nl * (sizeof(sw_result_t) + sizeof(uint32_t))));
-        sw_result_t *lout = (sw_result_t *)c->sh_out.p;
-        uint32_t *lidx = (uint32_t *)(lout + nl);
-        cudaStream_t s = c->stream;
-        r = shard_run(c, av.ptr, arena_bytes, pairs, n_pairs, d, n_devices, params, lout, lidx, s, tm);
-        if (r) return r;
-        // results back in input order: the shard's records and indices come
-        // down, the host scatters them into the caller's buffer
-        std::vector<sw_result_t> hout(nl);
-        std::vector<uint32_t> hidx(nl);
-        CU(cudaEventRecord(c->ev[10], s));
-        CU(cudaMemcpyAsync(hout.data(), lout, nl * sizeof(sw_result_t), cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(hidx.data(), lidx, nl * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        CU(cudaEventRecord(c->ev[11], s));
-        CU(cudaStreamSynchronize(s));
-        for (uint64_t r2 = 0; r2 < nl; ++r2) out[hidx[r2]] = hout[r2];
-        if (tm) {
-          tm->d2h_ms = ev_ms(c->ev[10], c->ev[11]);
-          tm->h2d_bytes = n_pairs * sizeof(sw_pair_t);
-          tm->d2h_bytes = nl * (sizeof(sw_result_t) + sizeof(uint32_t));
-        }
-        return SW_OK;
-      };
-      L.rc = body();
+      Lane &L = lanes[d];
+      // each GPU uploads only its range's pairs and the bytes they reference
+      // (overlapped with its forward pass) and writes its results straight
+      // into the caller's buffer: the ranges are contiguous in input order
+      L.rc = align_range(devices[d], arena, arena_bytes, pairs, b[d], b[d + 1], false, params,
+                         out + b[d], false, nullptr, tm);
       if (L.rc) L.err = g_err;
-      if (tm) tm->total_ms = now_ms() - t0;
+      if (tm) tm->host_plan_ms += plan_ms;
     });
   }
   for (auto &t : th) t.join();
@@ -1194,8 +1230,7 @@ void sw_release(int device) {
     for (DevBuf *b : {&c->arena, &c->codes, &c->pairs, &c->out, &c->st, &c->lists, &c->ctrs,
                       &c->stats, &c->bnd, &c->pool, &c->skeys, &c->svals, &c->cubtmp,
                       &c->km_arena, &c->km_off, &c->km_len, &c->km_base, &c->km_keys, &c->km_runs,
-                      &c->km_pairs, &c->km_out, &c->km_small, &c->cta_rows, &c->sh_pairs, &c->sh_keys,
-                      &c->sh_lpairs, &c->sh_lidx, &c->sh_llen, &c->sh_loff, &c->sh_arena, &c->sh_out})
+                      &c->km_pairs, &c->km_out, &c->km_small, &c->cta_rows, &c->sh_cells})
       b->release();
     c->pool_want = 0;
   }

@@ -124,7 +124,10 @@ struct KArgs {
   uint32_t *lists;         // [kStages][kNumClasses][n_pairs]
   uint32_t *ctrs;          // count[kStages*kNumClasses], cursor[...] after it
   uint64_t n_pairs;
-  uint64_t arena_bytes;     // pairs must lie inside [0, arena_bytes) (checked by k_classify)
+  uint64_t arena_bytes;     // pairs must lie inside [arena_lo, arena_bytes) (checked by k_classify)
+  uint64_t arena_lo;        // first valid arena offset: raw/codes are virtual bases such that
+                            // raw + off is valid for off in [arena_lo, arena_bytes) (a shard
+                            // of a batch uploads only that byte range)
   const uint8_t *lut;      // raw byte -> residue code (align.py:27-30), 256 entries
   // host-pipelined arenas: ready = number of arena slices of slice_bytes that
   // have landed (written by the copy stream); nullptr = arena fully resident
@@ -201,7 +204,7 @@ struct RawView {
 __device__ __forceinline__ void wait_arena(const KArgs &A, uint64_t end, int lane) {
   if (A.ready == nullptr || end == 0) return;
   if (lane == 0) {
-    const uint32_t need = (uint32_t)((end - 1) / A.slice_bytes + 1);
+    const uint32_t need = (uint32_t)((end - A.arena_lo - 1) / A.slice_bytes + 1);
     while (*A.ready < need) __nanosleep(256);
   }
   __syncwarp();
@@ -1304,6 +1307,7 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
     // scheduled; the call then fails with SW_EINVAL
     if (p.a_off > A.arena_bytes || p.a_len > A.arena_bytes - p.a_off ||   // no u64 wrap
         p.b_off > A.arena_bytes || p.b_len > A.arena_bytes - p.b_off ||
+        p.a_off < A.arena_lo || p.b_off < A.arena_lo ||
         p.a_len > 65000u || p.b_len > 65000u) {
       s.flags = kFlagInvalid;
       atomicAdd(&stats[5], 1ull);

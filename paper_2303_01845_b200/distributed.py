@@ -1,16 +1,16 @@
 """Multi-GPU shard / gather driver over torch.distributed (one process per GPU).
 
 The reference spreads a batch over process "lanes" with a contiguous ceil
-split (align.py:265-269), which leaves lanes imbalanced when lengths are
-skewed.  Here every rank holds the batch (host or device memory) and calls
-sw_align_shard with its rank: the GPU plans the cell-balanced partition
-itself (pairs in stable descending |a|*|b| order dealt in a snake over the
-ranks -- the same plan on every rank, no communication), pulls only its
-shard's sequence bytes (zero-copy from pinned host memory, or from device
-memory) and aligns them.  The per-rank 32-byte result records and their
-input positions are then gathered to one rank over NCCL (device tensors;
-NVLink) and scattered back into input order on that rank's GPU -- the only
-collective of the path.  gloo + a CPU `compute` stand-in serve the CPU tests.
+split by pair COUNT (align.py:265-269), which leaves lanes imbalanced when
+lengths are skewed.  Here every rank holds the batch (host or device memory)
+and calls sw_align_shard with its rank: the batch is cut into contiguous
+ranges of equal CELLS (|a|*|b|; sw_shard_ranges -- the same plan on every
+rank, no communication), each GPU uploads only its range's pairs and the
+bytes they reference (host memory, overlapped with its forward pass) or
+aligns them in place (device memory).  The per-rank 32-byte result records,
+contiguous in input order, are then gathered to one rank over NCCL (device
+tensors; NVLink) and concatenated there -- the only collective of the path.
+gloo + a CPU `compute` stand-in serve the CPU tests.
 """
 
 from typing import Callable, Optional
@@ -77,26 +77,52 @@ def gather_records(records: np.ndarray, index: np.ndarray, n_total: int, rank: i
 
 def gather_rows(rows, n_total: int, rank: int, world: int, dst: int = 0) -> Optional[np.ndarray]:
     """rows: [count, 9] int32 tensor (8 result words + input index) on the
-    communication device.  Pads to the largest shard, gathers to `dst` (NCCL:
-    device to device), scatters into input order there and returns the
-    records on dst's host (None elsewhere)."""
+    communication device, in any order.  Pads to the largest count, gathers
+    to `dst`, scatters into input order there; records on dst's host (None
+    elsewhere).  (The CPU-test path of align_distributed.)"""
     import torch
     import torch.distributed as dist
     dev = rows.device
-    cmax = max(_native.shard_count(n_total, world, r) for r in range(world)) if world else 0
-    cmax = max(cmax, int(rows.shape[0]))
-    buf = torch.full((cmax, 9), -1, dtype=torch.int32, device=dev)
+    cnt = torch.tensor([int(rows.shape[0])], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt)
+    cmax = max(int(c.item()) for c in counts)
+    buf = torch.full((max(cmax, 1), 9), -1, dtype=torch.int32, device=dev)
     buf[: rows.shape[0]] = rows
     parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
     dist.gather(buf, gather_list=parts, dst=dst)
     if rank != dst:
         return None
     allr = torch.cat(parts)
-    valid = allr[:, 8] >= 0
-    allr = allr[valid]
+    allr = allr[allr[:, 8] >= 0]
     out = torch.zeros((n_total, 8), dtype=torch.int32, device=dev)
     out[allr[:, 8].long()] = allr[:, :8]
     return out.cpu().numpy().view(RESULT_DTYPE).reshape(-1)
+
+
+def gather_ranges(rec, rank: int, world: int, dst: int = 0):
+    """rec: [count, 8] int32 device tensor holding this rank's records of its
+    contiguous range of the plan (ranks in input order).  NCCL gather to
+    `dst` (padded to the largest range), concatenated there: a [n, 8] int32
+    DEVICE tensor in input order on dst, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    dev = rec.device
+    cnt = torch.tensor([int(rec.shape[0])], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt)
+    counts = [int(c.item()) for c in counts]
+    cmax = max(max(counts), 1)
+    if rec.shape[0] == cmax:
+        buf = rec.contiguous()
+    else:
+        buf = torch.zeros((cmax, 8), dtype=torch.int32, device=dev)
+        buf[: rec.shape[0]] = rec
+    parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
+    dist.gather(buf, gather_list=parts, dst=dst)
+    if rank != dst:
+        return None
+    return torch.cat([p[:c] for p, c in zip(parts, counts)])
 
 
 def align_distributed(arena: np.ndarray, table: np.ndarray, params, rank: int, world: int,
@@ -115,15 +141,16 @@ def align_distributed(arena: np.ndarray, table: np.ndarray, params, rank: int, w
     import torch
     dev = torch.device("cuda", device)
     n = len(table)
-    nl = _native.shard_count(n, world, rank)
-    d_out = torch.empty((max(nl, 1), 9), dtype=torch.int32, device=dev)
-    d_idx = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+    bounds = _native.shard_ranges(table, world)
+    nl = int(bounds[rank + 1] - bounds[rank])
     res = torch.empty((max(nl, 1), 8), dtype=torch.int32, device=dev)
     arena = np.ascontiguousarray(arena, dtype=np.uint8)
     table = np.ascontiguousarray(table, dtype=PAIR_DTYPE)
-    _native.align_shard(arena.ctypes.data, arena.size, table.ctypes.data, n, rank, world, params,
-                        res.data_ptr(), d_idx.data_ptr(), device=device,
-                        stream=torch.cuda.current_stream(dev).cuda_stream)
-    d_out[:, :8] = res
-    d_out[:, 8] = d_idx
-    return gather_rows(d_out[:nl], n, rank, world, dst)
+    _, (first, end) = _native.align_shard(arena.ctypes.data, arena.size, table.ctypes.data, n,
+                                          rank, world, params, res.data_ptr(), device=device,
+                                          stream=torch.cuda.current_stream(dev).cuda_stream)
+    assert (first, end) == (int(bounds[rank]), int(bounds[rank + 1]))
+    out = gather_ranges(res[:nl], rank, world, dst)
+    if out is None:
+        return None
+    return out.cpu().numpy().view(RESULT_DTYPE).reshape(-1)

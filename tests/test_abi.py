@@ -44,31 +44,32 @@ def test_struct_layouts():
     assert ctypes.sizeof(_native.SwParams) == 8 + 625 * 4
 
 
-def test_partition_is_cell_balanced_snake():
+def test_partition_is_cell_balanced_contiguous():
+    """sw_shard_ranges / sw_partition_pairs: contiguous ranges of equal cells,
+    bounds[s] = min k with N * cells(pairs[0, k)) >= s * total."""
     rng = np.random.default_rng(0)
-    la = rng.integers(30, 2000, 5000)
-    lb = rng.integers(30, 2000, 5000)
-    _, t = pack_codes([b"A" * int(x) for x in la[:0]], [])  # empty table shape check
-    t = np.zeros(5000, dtype=_native.PAIR_DTYPE)
-    t["a_len"], t["b_len"] = la, lb
-    for world in (1, 2, 3, 8):
-        shard, load = _native.partition(t, world)
+    for n in (0, 1, 7, 5000, 300_000):
+        la = rng.integers(30, 2000, n)
+        lb = rng.integers(30, 2000, n)
+        t = np.zeros(n, dtype=_native.PAIR_DTYPE)
+        t["a_len"], t["b_len"] = la, lb
         cells = la.astype(np.int64) * lb
-        assert set(np.unique(shard)) <= set(range(world))
-        got = np.bincount(shard, weights=cells, minlength=world)
-        assert np.allclose(got, load.astype(np.float64))
-        # LPT bound: max load <= mean + largest item
-        assert got.max() <= cells.sum() / world + cells.max()
-        if world > 1:
-            assert (got.max() - got.mean()) / got.mean() < 0.01
-        # the rule (sw_shard.cuh): stable descending cells, snake deal
-        order = np.argsort(-cells, kind="stable")
-        r, q = np.arange(len(order)) // world, np.arange(len(order)) % world
-        expect = np.empty(len(order), np.int32)
-        expect[order] = np.where(r % 2 == 0, q, world - 1 - q)
-        assert (shard == expect).all()
-        for s_ in range(world):
-            assert _native.shard_count(len(t), world, s_) == int((shard == s_).sum())
+        pre = np.concatenate(([0], np.cumsum(cells)))
+        for world in (1, 2, 3, 8):
+            b = _native.shard_ranges(t, world)
+            total = int(pre[-1])
+            expect = [0] + [int(np.searchsorted(pre * world, s_ * total, side="left"))
+                            for s_ in range(1, world)] + [n]
+            if total == 0:
+                expect = [0] * world + [n]
+            assert b.tolist() == expect, (n, world)
+            shard, load = _native.partition(t, world)
+            got = np.bincount(shard, weights=cells, minlength=world) if n else np.zeros(world)
+            assert np.allclose(got, load.astype(np.float64))
+            for s_ in range(world):
+                assert (shard[b[s_]:b[s_ + 1]] == s_).all()
+            if n:
+                assert got.max() <= cells.sum() / world + cells.max()
 
 
 def test_no_cpu_fallback_without_gpu():

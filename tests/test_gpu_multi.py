@@ -1,8 +1,8 @@
-"""Multi-GPU path: device-planned cell-balanced shards, zero-copy shard
-gather, NCCL result gather (sw_align_shard, sw_align_batch_multi,
-distributed.align_distributed).  The shard tests run on one GPU (every
-shard of a 3-way split in turn); the multi-device ones need >= 2 GPUs
-(`gpurun --gpus 2`)."""
+"""Multi-GPU path: cell-balanced contiguous shards planned on the host or
+the device, range uploads, NCCL result gather (sw_align_shard,
+sw_align_batch_multi, distributed.align_distributed).  The shard tests run
+on one GPU (every shard of a 3-way split in turn); the multi-device ones
+need >= 2 GPUs (`gpurun --gpus 2`)."""
 
 import os
 import socket
@@ -41,33 +41,27 @@ def test_every_shard_of_a_split_is_exact(where):
     mat = matrix("blosum62")
     p = _native.make_params(11, 1, mat)
     ref, _ = _native.align_host(arena, table, p)
-    shard_host, load = _native.partition(table, 3)
+    bounds = _native.shard_ranges(table, 3)
     if where == "pinned":
         buf = _native.pinned_pool().acquire(arena.size)
         buf.array[:] = arena
-        src = buf.array
-        a_ptr, t_ptr = src.ctypes.data, table.ctypes.data
+        a_ptr, t_ptr = buf.array.ctypes.data, table.ctypes.data
     elif where == "pageable":
         a_ptr, t_ptr = arena.ctypes.data, table.ctypes.data
     else:
         d_a = torch.from_numpy(arena.copy()).cuda()
         d_t = torch.from_numpy(table.view(np.uint8).copy()).cuda()
         a_ptr, t_ptr = d_a.data_ptr(), d_t.data_ptr()
+        assert (_native.shard_ranges(t_ptr, 3, len(table)) == bounds).all()   # device plan
     got = np.zeros(len(table), dtype=_native.RESULT_DTYPE)
-    seen = np.zeros(len(table), dtype=np.int64)
+    d_out = torch.empty(len(table) * 32, dtype=torch.uint8, device="cuda")
     for s in range(3):
-        nl = _native.shard_count(len(table), 3, s)
-        d_out = torch.empty(nl * 32, dtype=torch.uint8, device="cuda")
-        d_idx = torch.empty(nl, dtype=torch.int32, device="cuda")
-        tm = _native.align_shard(a_ptr, arena.size, t_ptr, len(table), s, 3, p, d_out.data_ptr(),
-                                 d_idx.data_ptr())
-        idx = d_idx.cpu().numpy()
-        rec = d_out.cpu().numpy().view(_native.RESULT_DTYPE)
-        assert (shard_host[idx] == s).all()          # device plan == host plan
-        got[idx] = rec
-        seen[idx] += 1
-        assert tm["cells"] == int(load[s])
-    assert (seen == 1).all()
+        tm, (first, end) = _native.align_shard(a_ptr, arena.size, t_ptr, len(table), s, 3, p,
+                                               d_out.data_ptr())
+        assert (first, end) == (int(bounds[s]), int(bounds[s + 1]))
+        got[first:end] = d_out[: (end - first) * 32].cpu().numpy().view(_native.RESULT_DTYPE)
+        cells = int(np.dot(table["a_len"][first:end].astype(np.int64), table["b_len"][first:end]))
+        assert tm["cells"] == cells
     assert (got == ref).all()
     full = oracle.align_batch_c(arena, table, 11, 1, mat, threads=THREADS)
     assert (np.stack([got[f] for f in FIELDS], 1) == full[:, :7]).all()
@@ -80,10 +74,9 @@ def test_shard_of_invalid_pair_fails_the_call():
     bad["b_off"][17] = arena.size
     p = _native.make_params(11, 1, matrix("blosum62"))
     d_out = torch.empty(500 * 32, dtype=torch.uint8, device="cuda")
-    d_idx = torch.empty(500, dtype=torch.int32, device="cuda")
     with pytest.raises(ValueError):
         _native.align_shard(arena.ctypes.data, arena.size, bad.ctypes.data, len(bad), 0, 1, p,
-                            d_out.data_ptr(), d_idx.data_ptr())
+                            d_out.data_ptr())
 
 
 needs2 = pytest.mark.skipif("_native.device_count() < 2", reason="needs >= 2 GPUs")
