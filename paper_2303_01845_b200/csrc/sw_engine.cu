@@ -315,6 +315,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(cudaStreamWaitEvent(s, c->ev_in, 0));
   }
   uint32_t launches = 0;
+  uint32_t plan_cnt[kStages * kNumClasses];
   const double h0 = now_ms();
   // device buffers
   CU(c->codes.ensure(arena_bytes - arena_lo + 64));
@@ -407,6 +408,13 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
         A, (unsigned long long *)c->stats.p, env_ckpt && packed_ok, packed_ok, k_in, v_in, sort_cells);
     ++launches;
     CU(cudaGetLastError());
+    // the one host round trip of the call: which lists the plan filled, so
+    // the kernels of empty length classes and of an absent long-pair path are
+    // not launched (a persistent grid that finds its list empty still costs a
+    // launch and a wave of empty blocks: ~30 of a call's 38 launches on a
+    // one-class batch)
+    CU(cudaMemcpyAsync(plan_cnt, c->ctrs.p, sizeof(plan_cnt), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
     size_t tmp_bytes = 0;
     CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out,
                                        (int)n_pairs, 0, list_key_shift(sort_cells) + 7, s));
@@ -469,12 +477,22 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     for (int cls = 0; cls < kNumClasses; ++cls) {
       cudaStream_t cs = c->cstream[cls];
       CU(cudaStreamWaitEvent(cs, c->ev_fork, 0));
+      // round 0: classes the plan left empty are skipped; deferred rounds
+      // refill the lists on the device, so every class runs
+      if (pround == 0 && plan_cnt[6 * kNumClasses + cls] == 0) {
+        CU(cudaEventRecord(c->ev_k1[cls], cs));
+        CU(cudaEventRecord(c->ev_tb[cls], cs));
+        continue;
+      }
       c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, cs>>>(A, 6, cls);
       CU(cudaEventRecord(c->ev_k1[cls], cs));
       c->tb[cls].fn<<<c->tb[cls].grid, kTbWarps * 32, 0, cs>>>(A, 7, cls);
       CU(cudaEventRecord(c->ev_tb[cls], cs));
       launches += 2;
     }
+    // long pairs (one CTA per pair, or one warp per pair) exist only if the
+    // plan put some there; they all run in round 0
+    const bool long_pairs = pround == 0 && (plan_cnt[kCtaClass] + plan_cnt[kLongClass]) > 0;
     if (pround == 0 && arena_done) {
       // host-pipelined arena: the packed pass reads raw bytes through the
       // LUT; the scalar kernels below read the encoded arena once all of it
@@ -490,10 +508,12 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     // long pairs: scalar forward concurrently with the packed classes -- one
     // CTA per pair for pairs of >= 4 strips, one warp per pair for the others
     // (their lists are empty after the first round)
-    c->fwd_ctap.fn<<<c->fwd_ctap.grid, kCtaWarps * 32, c->fwd_ctap.smem, s>>>(A, 0, kCtaClass);
-    c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
-        A, 0, kLongClass);
-    launches += 2;
+    if (long_pairs) {
+      c->fwd_ctap.fn<<<c->fwd_ctap.grid, kCtaWarps * 32, c->fwd_ctap.smem, s>>>(A, 0, kCtaClass);
+      c->fwd[kLongClass].fn<<<c->fwd[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
+          A, 0, kLongClass);
+      launches += 2;
+    }
     CU(cudaEventRecord(c->ev[7], s));   // end of the concurrent scalar forward
     // then the packed pass's scalar fallbacks (their own list, complete once
     // every packed class has finished), on the long-pair kernel
@@ -505,19 +525,24 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
         A, 0, kFallbackClass);
     // long pairs the packed CTA kernel had no pool room for, then the j_end
     // replay of those it did
-    c->fwd_cta.fn<<<c->fwd_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 0, kCtaScalarClass);
-    c->jend.fn<<<c->jend.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 9, 0);
-    launches += 3;
+    ++launches;
+    if (long_pairs) {
+      c->fwd_cta.fn<<<c->fwd_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 0, kCtaScalarClass);
+      c->jend.fn<<<c->jend.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 9, 0);
+      launches += 2;
+    }
     c->fwd_wide.fn<<<c->fwd_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 3, 0);
     ++launches;
     CU(cudaGetLastError());
     CU(cudaEventRecord(c->ev[2], s));
+    // stage-1 lists: pairs of the scalar forwards (long pairs, and packed-pass
+    // fallbacks, whose end row can reach the CTA class) and of k_jend; wide
+    // pairs take the prefix box directly (no reverse pass)
     c->rev_cta.fn<<<c->rev_cta.grid, kCtaWarps * 32, kSmemCta, s>>>(A, 1, kCtaClass);
     ++launches;
     c->rev[kLongClass].fn<<<c->rev[kLongClass].grid, kWarpsPerBlock * 32, kSmemScore, s>>>(
         A, 1, kLongClass);
-    c->rev_wide.fn<<<c->rev_wide.grid, kWarpsPerBlock * 32, kSmemScore, s>>>(A, 4, 0);
-    launches += 2;
+    ++launches;
     CU(cudaGetLastError());
     CU(cudaEventRecord(c->ev[3], s));
     for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_tb[cls], 0));
