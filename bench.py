@@ -52,7 +52,7 @@ WORKLOADS = {
     "config5": {"pairs": 10_000,
                 "desc": "config 5: 10k pairs/GPU, lengths U[2000, 35000] (independent), "
                         "BLOSUM62, gap 11/1",
-                "cpu_sample": 24, "ref_sample": 2},
+                "cpu_sample": 4, "ref_sample": 1},
 }
 DTYPE = "int16x2 (biased u16x2 DPX lanes, exact; int32 re-run on overflow)"
 
@@ -331,7 +331,8 @@ def main():
                              f"{cores} forked lanes; {rn['seconds']:.1f} s wall",
                    "alignments_per_sec": rn["aln_per_s"],
                    "c_oracle_gcups": rc["gcups"],
-                   "c_oracle_note": f"plain-C restatement (oracle/sw_oracle.c), {rc['cores']} "
+                   "c_oracle_note": f"plain-C restatement (oracle/sw_oracle.c, "
+                                    f"{rc.get('restatement', 'orc_align')}), {rc['cores']} "
                                     f"pthreads, first {rc['pairs']} pairs"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GCUPS", "cores": None, "kind": "port",

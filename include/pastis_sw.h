@@ -83,7 +83,8 @@ typedef struct sw_result_t { /* AlignmentResult fields, 0-based inclusive spans 
 typedef struct sw_timing_t { /* filled when non-NULL; device times from CUDA events */
   double forward_ms;       /* K1: forward score + end cell (paper's "forward scoring time") */
   double reverse_ms;       /* K2: reverse pass -> start box */
-  double traceback_ms;     /* K3 + walk: box recompute with direction codes + traceback */
+  double traceback_ms;     /* K3 + walk: box recompute with direction codes + traceback
+                              (after the tile traceback K5, which is tile_tb_ms) */
   double kernel_ms;        /* all device work of the call (encode .. walk) */
   double h2d_ms;           /* host->device copies (host-buffer entry points only) */
   double d2h_ms;           /* device->host copy of the results */

@@ -316,6 +316,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   }
   uint32_t launches = 0;
   uint32_t plan_cnt[kStages * kNumClasses];
+  unsigned long long plan_ckpt = 0;   // checkpoint bytes the packed pass will need
   const double h0 = now_ms();
   // device buffers
   CU(c->codes.ensure(arena_bytes - arena_lo + 64));
@@ -414,6 +415,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     // launch and a wave of empty blocks: ~30 of a call's 38 launches on a
     // one-class batch)
     CU(cudaMemcpyAsync(plan_cnt, c->ctrs.p, sizeof(plan_cnt), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&plan_ckpt, (unsigned long long *)c->stats.p + 6, 8, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     size_t tmp_bytes = 0;
     CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out,
@@ -440,6 +442,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     const char *e = getenv("PASTIS_SW_POOL_MB");
     return e ? atoll(e) : 0ll;
   }();
+  // size the pool for this call's checkpoints up front (k_classify's
+  // estimate + 15 %), so the packed pass normally runs in one round; a pool
+  // that still overflows defers pairs to further rounds
+  if (env_mb == 0)
+    c->pool_want = std::max(c->pool_want, (size_t)(plan_ckpt + plan_ckpt / 7) + ((size_t)64 << 20));
   if (c->pool.bytes == 0 || c->pool_want > c->pool.bytes) {
     size_t free_b = 0, total_b = 0;
     CU(cudaMemGetInfo(&free_b, &total_b));
@@ -546,6 +553,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     CU(cudaGetLastError());
     CU(cudaEventRecord(c->ev[3], s));
     for (int cls = 0; cls < kNumClasses; ++cls) CU(cudaStreamWaitEvent(s, c->ev_tb[cls], 0));
+    CU(cudaEventRecord(c->ev[13], s));   // box traceback starts once every class's K5 is done
     uint32_t last_retry = 0;
     for (int round = 0;; ++round) {
       for (int cls = 0; cls < kNumClasses; ++cls) {
@@ -558,7 +566,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
       CU(cudaEventRecord(c->ev[4], s));
       CU(cudaMemcpyAsync(h_cnt, c->ctrs.p, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
-      tb_ms += ev_ms(round == 0 ? c->ev[3] : c->ev[5], c->ev[4]);
+      tb_ms += ev_ms(round == 0 ? c->ev[13] : c->ev[5], c->ev[4]);
       const uint32_t n_retry = h_cnt[5 * kNumClasses];
       if (n_retry == 0) break;
       // every retry round starts on an empty pool, so it places at least one

@@ -1336,15 +1336,27 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
   }
   unsigned long long c = real ? cells : 0ull;
   unsigned long long mb = real ? p.b_len : 0ull;
+  // checkpoint bytes the packed pass will ask for (per pair: its column
+  // checkpoints and half of its duo's row checkpoints), so the host can size
+  // the pool before the first packed round instead of deferring pairs
+  unsigned long long ck = 0ull;
+  if (real && fused) {
+    const int R = class_rows(packed_class_of((int)p.a_len, (int)p.b_len));
+    const CkLayout L = ck_layout(R, (int)p.b_len);
+    const unsigned long long strips = (p.a_len + 32u * R - 1) / (32u * R);
+    ck = strips * (L.col_words + L.row_words / 2) * 4ull;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     c += __shfl_xor_sync(0xffffffffu, c, o);
+    ck += __shfl_xor_sync(0xffffffffu, ck, o);
     const unsigned long long t = __shfl_xor_sync(0xffffffffu, mb, o);
     mb = t > mb ? t : mb;
   }
   if (lane == 0) {
     if (c) atomicAdd(&stats[0], c);
     if (mb) atomicMax(&stats[1], mb);
+    if (ck) atomicAdd(&stats[6], ck);
   }
 }
 

@@ -17,9 +17,9 @@ N="ncu --clock-control none"
 timeout 900 $N --metrics gpu__time_duration.sum --csv --log-file $OUT/launches_config3.csv \
     $CMD > $OUT/ncu_launches.log 2>&1
 timeout 900 $N --set full --import-source on --kernel-name-base mangled \
-    -k "regex:k_score_packedILi9E" -s 3 -c 1 -o $OUT/prof_k1p9 $CMD > $OUT/ncu_k1p.log 2>&1
+    -k "regex:k_score_packedILi9E" -s 1 -c 1 -o $OUT/prof_k1p9 $CMD > $OUT/ncu_k1p.log 2>&1
 timeout 900 $N --set full --import-source on --kernel-name-base mangled \
-    -k "regex:k_tbILi9E" -s 3 -c 1 -o $OUT/prof_k5_9 $CMD > $OUT/ncu_k5.log 2>&1
+    -k "regex:k_tbILi9E" -s 1 -c 1 -o $OUT/prof_k5_9 $CMD > $OUT/ncu_k5.log 2>&1
 CMD5="python bench.py --workload config5 --pairs 600 --steps 1 --warmup 1 --no-cpu-baseline --no-api"
 timeout 600 $CMD5 > $OUT/plain5.json 2>&1 && \
 timeout 900 $N --metrics gpu__time_duration.sum --csv --log-file $OUT/launches_config5.csv \
