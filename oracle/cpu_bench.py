@@ -106,6 +106,9 @@ def main():
     ap.add_argument("--pairs", type=int, default=2000)
     ap.add_argument("--seed", type=int, default=2303)
     ap.add_argument("--offset", type=int, default=0)
+    ap.add_argument("--pairs-file", default=None,
+                    help="npz with `arena` (uint8) and `table` (a_off, b_off, a_len, b_len): time "
+                         "exactly these pairs (e.g. a pipeline's candidate pairs)")
     ap.add_argument("--procs", type=int, default=0)
     ap.add_argument("--gap-open", type=int, default=11)
     ap.add_argument("--gap-extend", type=int, default=1)
@@ -113,7 +116,13 @@ def main():
     procs = args.procs or len(os.sched_getaffinity(0))
     from paper_2303_01845_b200 import blosum62
     mat = np.asarray(blosum62.MATRIX, dtype=np.int32)
-    pairs = sample_pairs(args.workload, args.pairs, args.seed, args.offset)
+    if args.pairs_file:
+        z = np.load(args.pairs_file)
+        raw = z["arena"].tobytes()
+        pairs = [(raw[a:a + la].decode(), raw[b:b + lb].decode())
+                 for a, b, la, lb in z["table"].tolist()]
+    else:
+        pairs = sample_pairs(args.workload, args.pairs, args.seed, args.offset)
     gap = (args.gap_open, args.gap_extend)
     if args.mode == "numpy":
         r = time_numpy(pairs, gap, mat, procs)

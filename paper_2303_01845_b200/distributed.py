@@ -22,7 +22,7 @@ from ._native import PAIR_DTYPE, RESULT_DTYPE
 
 
 def partition(table: np.ndarray, world: int) -> np.ndarray:
-    """Shard id per pair (LPT over cells, C++ sw_partition_pairs)."""
+    """Shard id per pair (the cell-balanced contiguous plan, sw_partition_pairs)."""
     shard, _ = _native.partition(table, world)
     return shard
 

@@ -43,6 +43,7 @@ class PipelineConfig:
     kmer: KmerParams = field(default_factory=KmerParams)
     align: AlignParams = field(default_factory=AlignParams)
     devices: Optional[tuple] = None
+    blocks: int = 4       # pre-blocking: alignment blocks (one in flight beside the host filter)
 
 
 @dataclass
@@ -100,35 +101,56 @@ def run_search(config, input_path, output_path) -> RunStats:
     table = arena_pairs(fa, ii, jj)
     p = _native_params(aparams) if isinstance(aparams, AlignParams) else _native.make_params(
         aparams.gap_open, aparams.gap_extend, np.asarray(aparams.matrix, dtype=np.int32))
-    if len(table) == 0:
-        rec, tms = np.empty(0, dtype=_native.RESULT_DTYPE), []
-    elif len(devices) == 1:
-        rec, tm = _native.align_host(fa.arena, table, p, device=devices[0])
-        tms = [tm]
-    else:
-        rec, tms = _native.align_multi(fa.arena, table, p, devices)
-    bad = np.flatnonzero(rec["status"] != 0) if len(rec) else []
-    if len(bad):
-        k = int(bad[0])
-        raise PipelineError(f"stage align: pair ({int(ii[k])}, {int(jj[k])}): status "
-                            f"{int(rec['status'][k])}")
-    accept, identity, cov_a, cov_b = evaluate_records(
-        ii, jj, table["a_len"], table["b_len"], rec, aparams.min_identity, aparams.min_coverage)
-    align_s = perf_counter() - t0
+    headers = fa.headers
+    # Pre-blocking (pipeline.py:209-212, 305-314): the candidate list is cut
+    # into blocks; the GPU aligns block b+1 (a host thread: the ctypes call
+    # releases the GIL) while this thread filters and formats block b's edges.
+    n_blocks = max(1, min(int(getattr(config, "blocks", 4)), len(table) // 20000 or 1))
+    bounds = np.linspace(0, len(table), n_blocks + 1).astype(np.int64)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def align_block(b):
+        sub = table[bounds[b]:bounds[b + 1]]
+        if len(sub) == 0:
+            return np.empty(0, dtype=_native.RESULT_DTYPE), []
+        if len(devices) == 1:
+            r, tm = _native.align_host(fa.arena, sub, p, device=devices[0])
+            return r, [tm]
+        return _native.align_multi(fa.arena, sub, p, devices)
+
+    lines, tms, io_w, per_dev = [], [], 0.0, {}
+    with ThreadPoolExecutor(max_workers=1, thread_name_prefix="pastis-align") as pool:
+        fut = pool.submit(align_block, 0)
+        for b in range(n_blocks):
+            rec_b, tms_b = fut.result()
+            if b + 1 < n_blocks:
+                fut = pool.submit(align_block, b + 1)     # in flight while we filter block b
+            tms += tms_b
+            for d_i, t in enumerate(tms_b):
+                per_dev[d_i] = per_dev.get(d_i, 0.0) + t["forward_ms"]
+            s0, s1 = int(bounds[b]), int(bounds[b + 1])
+            bad = np.flatnonzero(rec_b["status"] != 0) if len(rec_b) else []
+            if len(bad):
+                k = s0 + int(bad[0])
+                raise PipelineError(f"stage align: pair ({int(ii[k])}, {int(jj[k])}): status "
+                                    f"{int(rec_b['status'][k - s0])}")
+            tw = perf_counter()
+            accept, identity, cov_a, cov_b = evaluate_records(
+                ii[s0:s1], jj[s0:s1], table["a_len"][s0:s1], table["b_len"][s0:s1], rec_b,
+                aparams.min_identity, aparams.min_coverage)
+            for k in np.flatnonzero(accept).tolist():
+                e = SimilarityEdge(int(ii[s0 + k]), int(jj[s0 + k]), int(rec_b["score"][k]),
+                                   float(identity[k]), float(cov_a[k]), float(cov_b[k]))
+                lines.append(format_edge_line(e, headers))
+            io_w += perf_counter() - tw
+    align_s = perf_counter() - t0 - io_w
 
     t0 = perf_counter()
-    headers = fa.headers
-    n_out = 0
     with open(output_path, "w", encoding="utf-8", newline="\n") as fh:
-        lines = []
-        for k in np.flatnonzero(accept).tolist():
-            e = SimilarityEdge(int(ii[k]), int(jj[k]), int(rec["score"][k]), float(identity[k]),
-                               float(cov_a[k]), float(cov_b[k]))
-            lines.append(format_edge_line(e, headers))
         if lines:
             fh.write("\n".join(lines) + "\n")
-        n_out = len(lines)
-    io_s += perf_counter() - t0
+    n_out = len(lines)
+    io_s += io_w + perf_counter() - t0
 
     total = perf_counter() - t_start
     cells = int(np.sum(table["a_len"].astype(np.int64) * table["b_len"].astype(np.int64)))
@@ -150,10 +172,10 @@ def run_search(config, input_path, output_path) -> RunStats:
         total_seconds=total,
         alignments_per_second=(int(kst["performed"]) / total) if total > 0 else 0.0,
         cups=(cells / kernel_s) if kernel_s > 0 else 0.0,
-        imbalance_align_pct=_imbalance([t["forward_ms"] for t in tms]),
+        imbalance_align_pct=_imbalance(list(per_dev.values())),
         imbalance_sparse_pct=0.0,
         compression_factor=(int(kst["flops"]) / overlap_nnz) if overlap_nnz else 0.0,
-        peak_live_blocks=1 if len(table) else 0,
+        peak_live_blocks=min(2, n_blocks) if len(table) else 0,
     )
 
 

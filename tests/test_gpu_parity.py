@@ -420,3 +420,37 @@ print(json.dumps({"bad": int((got != ref[:, :7]).any(axis=1).sum())}))
                          text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
     assert json.loads(out.stdout.strip().splitlines()[-1])["bad"] == 0
+
+
+def test_lookahead_loop_with_batches_in_flight():
+    """The reference pipeline's pre-blocking loop (pipeline.py:209-240,
+    305-314: submit a block, drain while more than `lookahead` are in flight,
+    drain the rest) against AlignEngine with use_processes=True: config 1's
+    628 pairs in 7 blocks, up to 3 batches submitted before the first
+    result() -- the next block packs on the host while the GPU aligns the
+    previous one; the canonical output is the reference's."""
+    from collections import deque
+    d = load_golden("config1.json")
+    res = d["residues"]
+    params = sw.AlignParams()
+    blocks = [d["pairs"][k:k + 97] for k in range(0, len(d["pairs"]), 97)]
+    lines, inflight, capacity, max_inflight = [], deque(), 2, 0
+    with sw.AlignEngine(params, lanes=1, use_processes=True) as eng:
+        def drain_one():
+            pairs, pending = inflight.popleft()
+            results, errors, counters, lanes = pending.result()
+            assert not errors and counters.alignments == len(pairs)
+            for (i, j), r in zip(pairs, results):
+                edge = sw.evaluate_pair(i, j, res[i], res[j], r, params)
+                if edge is not None:
+                    lines.append(sw.format_edge_line(edge, d["headers"]))
+        for pairs in blocks:
+            batch = [(res[i], res[j], None) for i, j in pairs]
+            inflight.append((pairs, eng.submit(batch)))
+            max_inflight = max(max_inflight, len(inflight))
+            while len(inflight) > capacity:
+                drain_one()
+        while inflight:
+            drain_one()
+    assert max_inflight == capacity + 1
+    assert hashlib.sha256(sw.canonical_bytes(lines)).hexdigest() == d["canonical_sha256"]

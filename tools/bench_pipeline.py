@@ -4,13 +4,21 @@ stage (RunStats) after one warm-up run, with the canonical digest checked
 against the reference's (a841c454...).  The reference's own
 run of the same config took 935 s on 8 cores.
 
-    python tools/bench_pipeline.py [count seed]
+    python tools/bench_pipeline.py [count seed] [--cpu-baseline]
+
+--cpu-baseline also times the reference ALGORITHM's alignment stage on the
+box's host cores over exactly the pipeline's SW pairs (the numpy
+restatement of align.py:79-181 in forked lanes, oracle/cpu_bench.py), for
+the GPU-vs-CPU comparison of this config's alignment stage.
 """
 import json
 import os
+import subprocess
 import sys
 import tempfile
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -21,9 +29,29 @@ REF_DIGEST = {(100_000, 4): "a841c454a5f50663d63d91985af2dda1ae888eb0d1bea62d095
               (1000, 0): "e08ae282e079121bf115d332ba6dd79838dd2b4811c8fefd2ce39c66cbdfe655"}
 
 
+def cpu_align_baseline(fa_path, td):
+    """The reference algorithm (numpy port, forked lanes) over the pipeline's
+    candidate pairs, in a fresh process."""
+    from paper_2303_01845_b200 import seqio
+    from paper_2303_01845_b200.candidates import KmerParams, kmer_candidates
+    fa = seqio.read_fasta_arena(fa_path)
+    cand, _ = kmer_candidates(fa, KmerParams())
+    table = seqio.arena_pairs(fa, cand["i"].astype(np.int64), cand["j"].astype(np.int64))
+    path = os.path.join(td, "pairs.npz")
+    np.savez(path, arena=np.asarray(fa.arena), table=table)
+    out = subprocess.run([sys.executable, "-m", "oracle.cpu_bench", "--mode", "numpy",
+                          "--pairs-file", path, "--gap-open", "11", "--gap-extend", "2"],
+                         cwd=ROOT, capture_output=True, text=True, check=True)
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    r["note"] = ("numpy restatement of align.py:79-181 (the reference algorithm) over the "
+                 "pipeline's SW pairs, forked lanes on the host cores")
+    return r
+
+
 def main():
-    count = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000
-    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    count = int(args[0]) if len(args) > 0 else 100_000
+    seed = int(args[1]) if len(args) > 1 else 4
     with tempfile.TemporaryDirectory() as td:
         fa = os.path.join(td, "in.fa")
         t0 = time.perf_counter()
@@ -40,6 +68,8 @@ def main():
         best["digest_matches_reference"] = best["digest"] == REF_DIGEST.get((count, seed))
         best["corpus"] = {"count": count, "seed": seed, "generate_s": gen_s,
                           "fasta_mb": os.path.getsize(fa) / 1e6}
+        if "--cpu-baseline" in sys.argv:
+            best["cpu_align_baseline"] = cpu_align_baseline(fa, td)
         print(json.dumps(best))
 
 
