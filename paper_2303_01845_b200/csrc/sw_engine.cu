@@ -401,10 +401,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     uint32_t *v_in = (uint32_t *)c->svals.p, *v_out = v_in + n_pairs;
     // work lists sorted by shape (m, n descending) by default;
     // PASTIS_SW_SORT=cells sorts by cell count instead (A/B comparisons)
-    static const int sort_cells = [] {
+    static const int env_sort = [] {
       const char *e = getenv("PASTIS_SW_SORT");
-      return (e && strcmp(e, "cells") == 0) ? 1 : 0;
+      return (e && strcmp(e, "cells") == 0) ? 1 : (e && strcmp(e, "chunk") == 0) ? 2 : 0;
     }();
+    const int sort_cells = env_sort == 2 ? (ready ? 2 : 0) : env_sort;
     k_classify<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
         A, (unsigned long long *)c->stats.p, env_ckpt && packed_ok, packed_ok, k_in, v_in, sort_cells);
     ++launches;

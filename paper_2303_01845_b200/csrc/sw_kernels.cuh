@@ -1327,10 +1327,18 @@ __global__ void k_classify(KArgs A, unsigned long long *stats, int allow_ckpt, i
   const int leader = __ffs(peers) - 1;
   if (slot >= 0 && (int)lane == leader) atomicAdd(&A.ctrs[slot], (uint32_t)__popc(peers));
   if (in) {
-    const unsigned long long order =
-        sort_cells ? ((0xFFFFFFFFFFFFull - cells) & 0xFFFFFFFFFFFFull)
-                   : (((unsigned long long)(0xFFFFu - min(p.a_len, 0xFFFFu)) << 16) |
-                      (unsigned long long)(0xFFFFu - min(p.b_len, 0xFFFFu)));
+    const unsigned long long shape = (((unsigned long long)(0xFFFFu - min(p.a_len, 0xFFFFu)) << 16) |
+                                      (unsigned long long)(0xFFFFu - min(p.b_len, 0xFFFFu)));
+    // sort_cells 2 (host-pipelined arenas): the upload slice the pair's bytes
+    // end in, then shape -- the packed pass consumes the arena roughly in
+    // upload order, so its warps rarely wait for late slices
+    unsigned long long order = shape;
+    if (sort_cells == 1) order = (0xFFFFFFFFFFFFull - cells) & 0xFFFFFFFFFFFFull;
+    if (sort_cells == 2 && A.slice_bytes) {
+      const uint64_t end = max(p.a_off + p.a_len, p.b_off + p.b_len);
+      const uint64_t chunk = end > A.arena_lo ? (end - A.arena_lo - 1) / A.slice_bytes : 0;
+      order = (min(chunk, (uint64_t)0xFFFF) << 32) | shape;
+    }
     keys[k] = ((unsigned long long)(slot >= 0 ? slot : kNoList) << list_key_shift(sort_cells)) | order;
     vals[k] = (uint32_t)k;
   }
