@@ -355,12 +355,6 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   A.lut = (const uint8_t *)c->lut.p;
   A.ready = ready;
   A.slice_bytes = slice_bytes;
-  // host-pipelined arena: K1p defers duos whose slices are still in flight
-  // to per-class late lists (slots pre-filled with kLateEmpty)
-  A.late = ready != nullptr ? 1 : 0;
-  if (A.late)
-    CU(cudaMemsetAsync((uint32_t *)c->lists.p + (size_t)kLateStage * kNumClasses * n_pairs, 0xFF,
-                       (size_t)kNumClasses * n_pairs * 4, s));
   A.cta_rows = (uint2 *)c->cta_rows.p;
   A.open_ = prm->gap_open;
   A.ext = prm->gap_extend;
@@ -482,7 +476,6 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   for (int pround = 0;; ++pround) {
     CU(cudaMemsetAsync(A.pool_top, 0, 8, s));
     if (pround > 0) {
-      A.late = 0;   // the arena has landed by now (and the late lists are not reset)
       k_packed_round<<<kNumClasses, 256, 0, s>>>(A);
       ++launches;
     }

@@ -58,14 +58,10 @@ __host__ __device__ inline int long_class(int m, bool packed_ok = true) {
   return packed_ok && (m + 32 * kCtaRowsR - 1) / (32 * kCtaRowsR) >= kCtaStripsMin ? kCtaClass
                                                                                     : kLongClass;
 }
-constexpr int kStages = 12; // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
+constexpr int kStages = 10; // 0 K1, 1 K2, 2 K3, 3 K1-wide, 4 K2-wide, 5 retry,
                             // 6 K1 with checkpoints, 7 tile traceback,
                             // 8 K1 with checkpoints deferred to the next round (pool full),
-                            // 9 j_end replay of the packed long-pair forward (k_jend),
-                            // 10 K1 with checkpoints whose arena bytes had not landed (late),
-                            // 11 (counter only) main-list items resolved by K1p
-constexpr int kLateStage = 10, kResolvedStage = 11;
-constexpr uint32_t kLateEmpty = 0xFFFFFFFFu, kLateNone = 0xFFFFFFFEu;
+                            // 9 j_end replay of the packed long-pair forward (k_jend)
 constexpr uint64_t kFusedMaxCells = 1ull << 22;  // pairs up to 2048x2048 take the fused path
 constexpr int32_t kScaledLimit = 32767 - 128;
 constexpr int32_t kNegInf = -(1 << 30);
@@ -137,7 +133,6 @@ struct KArgs {
   // have landed (written by the copy stream); nullptr = arena fully resident
   const volatile uint32_t *ready;
   uint64_t slice_bytes;
-  int32_t late;             // K1p may defer duos whose slices have not landed (round 0, host arena)
   uint2 *cta_rows;         // K1cp: per-CTA ring of strip bottom rows (sw_cta_packed.cuh)
   int2 *bnd;               // per-warp strip boundary rows
   uint64_t bnd_stride;     // int2 per warp

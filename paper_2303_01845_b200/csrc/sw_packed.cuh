@@ -225,86 +225,19 @@ k_score_packed(KArgs A, int stage, int cls) {
   const uint32_t NEG2 = A.p_ext2;                      // biased "-inf": E/F - ext == 0
   const uint32_t HO0 = A.p_ho0;                        // biased H - open for H == 0
   const uint32_t NEXT2 = A.p_next2, NOPEN2 = A.p_nopen2;  // per-half -ext, -open
-  // Host-pipelined arena (A.late): a duo whose bytes have not all landed yet
-  // is not waited for but moved to the class's late list (stage kLateStage),
-  // which the warps drain once the main list is claimed -- the main list is
-  // ordered by shape, so its first duos touch the whole arena and would
-  // otherwise hold their SMs until the upload ends.  Late-list slots are
-  // pre-filled with kLateEmpty and written by the deferring warp; the drain
-  // ends when every main item has been resolved (processed or deferred) and
-  // the late list has no unclaimed slot.
-  volatile uint32_t *late_cnt = &A.ctrs[kLateStage * kNumClasses + cls];
-  volatile uint32_t *resolved = &A.ctrs[kResolvedStage * kNumClasses + cls];
-  uint32_t *late_list = list_of(A, kLateStage, cls);
-  bool late_mode = false;
   for (;;) {
     // two consecutive work items per warp
     uint32_t pos = 0;
-    int64_t kk[2] = {-1, -1};
-    if (!late_mode) {
-      if (lane == 0) pos = atomicAdd(&A.ctrs[kStages * kNumClasses + stage * kNumClasses + cls], 2u);
-      pos = __shfl_sync(0xffffffffu, pos, 0);
-      const uint32_t cnt = *(volatile uint32_t *)&A.ctrs[stage * kNumClasses + cls];
-      if (pos >= cnt) {
-        if (!A.late) break;
-        late_mode = true;
-        continue;
-      }
-      kk[0] = (int64_t)list_of(A, stage, cls)[pos];
-      kk[1] = pos + 1 < cnt ? (int64_t)list_of(A, stage, cls)[pos + 1] : -1;
-      if (A.late) {
-        uint64_t end = 0;
-        for (int h = 0; h < 2; ++h)
-          if (kk[h] >= 0) {
-            const sw_pair_t p = A.pairs[kk[h]];
-            end = max(end, max(p.a_off + p.a_len, p.b_off + p.b_len));
-          }
-        int ready = 1;
-        if (lane == 0) {
-          const uint32_t need = (uint32_t)((end - A.arena_lo - 1) / A.slice_bytes + 1);
-          ready = *A.ready >= need;
-          const uint32_t items = kk[1] >= 0 ? 2u : 1u;
-          if (!ready) {
-            const uint32_t q = atomicAdd((uint32_t *)late_cnt, 2u);
-            late_list[q] = (uint32_t)kk[0];
-            late_list[q + 1] = kk[1] >= 0 ? (uint32_t)kk[1] : kLateNone;
-            __threadfence();
-          }
-          atomicAdd((uint32_t *)resolved, items);
-        }
-        if (!__shfl_sync(0xffffffffu, ready, 0)) continue;
-      }
-    } else {
-      int done = 0;
-      if (lane == 0) {
-        pos = atomicAdd(&A.ctrs[kStages * kNumClasses + kLateStage * kNumClasses + cls], 2u);
-        const uint32_t main_cnt = *(volatile uint32_t *)&A.ctrs[stage * kNumClasses + cls];
-        for (;;) {
-          if (*late_cnt > pos) break;
-          if (*resolved >= main_cnt) {
-            __threadfence();
-            if (*late_cnt <= pos) done = 1;
-            break;
-          }
-          __nanosleep(500);
-        }
-        if (!done) {
-          uint32_t a, b;
-          while ((a = *(volatile uint32_t *)&late_list[pos]) == kLateEmpty) __nanosleep(100);
-          while ((b = *(volatile uint32_t *)&late_list[pos + 1]) == kLateEmpty) __nanosleep(100);
-          kk[0] = a;
-          kk[1] = b == kLateNone ? -1 : (int64_t)b;
-        }
-      }
-      if (__shfl_sync(0xffffffffu, done, 0)) break;
-      kk[0] = __shfl_sync(0xffffffffu, kk[0], 0);
-      kk[1] = __shfl_sync(0xffffffffu, kk[1], 0);
-    }
+    if (lane == 0) pos = atomicAdd(&A.ctrs[kStages * kNumClasses + stage * kNumClasses + cls], 2u);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const uint32_t cnt = *(volatile uint32_t *)&A.ctrs[stage * kNumClasses + cls];
+    if (pos >= cnt) break;
     PackedPair P[2];
     uint64_t arena_end = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      P[h].k = kk[h];
+      const uint32_t idx = pos + h;
+      P[h].k = idx < cnt ? (int64_t)list_of(A, stage, cls)[idx] : -1;
       if (P[h].k >= 0) {
         const sw_pair_t p = A.pairs[P[h].k];
         arena_end = max(arena_end, max(p.a_off + p.a_len, p.b_off + p.b_len));
