@@ -92,6 +92,9 @@ struct DeviceCtx {
   // sharding (sw_align_shard / sw_align_batch_multi): the whole pair table,
   // sort keys, the shard's pair table / indices / lengths / offsets, its arena
   DevBuf sh_cells;
+  // gathered host arenas: per-pair ready flags, gather segments, their stream
+  DevBuf pready, gseg;
+  cudaStream_t gstream = nullptr;
   DevBuf skeys, svals, cubtmp;  // work-list sort
   DevBuf km_arena, km_off, km_len, km_base, km_keys, km_runs, km_pairs, km_out, km_small;
   cudaEvent_t ev[16];
@@ -223,6 +226,7 @@ int get_ctx(int device, DeviceCtx **out) {
       CU(cudaEventCreate(&c->ev_tb[k]));
     }
     CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithPriority(&c->gstream, cudaStreamNonBlocking, prio_greatest));
     CU(cudaEventCreateWithFlags(&c->ev_pairs, cudaEventDisableTiming));
     CU(cudaEventCreate(&c->ev_arena));
     CU(c->readyb.ensure(64));
@@ -304,7 +308,8 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
                const sw_pair_t *d_pairs, uint64_t n_pairs, const sw_params_t *prm,
                sw_result_t *d_out, cudaStream_t s, sw_timing_t *tm,
                const uint32_t *ready = nullptr, uint64_t slice_bytes = 0,
-               cudaEvent_t arena_done = nullptr, uint64_t arena_lo = 0) {
+               cudaEvent_t arena_done = nullptr, uint64_t arena_lo = 0,
+               const uint8_t *gather_src = nullptr) {
   if (n_pairs == 0) return SW_OK;
   if (n_pairs > 0xFFFFFFF0ull) return fail(SW_EINVAL, "too many pairs in one call");
   // the chain runs on the greatest-priority stream, joined back to `s` at the end
@@ -355,6 +360,13 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   A.lut = (const uint8_t *)c->lut.p;
   A.ready = ready;
   A.slice_bytes = slice_bytes;
+  // gathered host arena: the pair's bytes are pulled over PCIe by
+  // k_gather_arena in consumption order; K1p waits per duo on its flags
+  if (gather_src) {
+    CU(c->pready.ensure(n_pairs * 4));
+    CU(cudaMemsetAsync(c->pready.p, 0, n_pairs * 4, s));
+    A.pair_ready = (const uint32_t *)c->pready.p;
+  }
   A.cta_rows = (uint2 *)c->cta_rows.p;
   A.open_ = prm->gap_open;
   A.ext = prm->gap_extend;
@@ -429,6 +441,38 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
                       0, s>>>(A, k_out, v_out, list_key_shift(sort_cells));
     ++launches;
     CU(cudaGetLastError());
+    if (gather_src) {
+      // gather order: kGatherRounds rounds through every packed class list
+      // (the classes run concurrently, each at its own pace through its
+      // list), then the long-pair lists (whose kernels wait for all of it)
+      constexpr int kGatherRounds = 64;
+      std::vector<GatherSeg> seg;
+      uint32_t total = 0;
+      for (int r = 0; r < kGatherRounds; ++r)
+        for (int cls = 0; cls < kNumClasses; ++cls) {
+          const uint32_t cnt = plan_cnt[6 * kNumClasses + cls];
+          const uint32_t j0 = (uint32_t)((uint64_t)cnt * r / kGatherRounds);
+          const uint32_t j1 = (uint32_t)((uint64_t)cnt * (r + 1) / kGatherRounds);
+          if (j1 > j0) { seg.push_back({(uint32_t)(6 * kNumClasses + cls), j0, total}); total += j1 - j0; }
+        }
+      for (int cls = 0; cls < kNumClasses; ++cls) {
+        const uint32_t cnt = plan_cnt[cls];
+        if (cnt) { seg.push_back({(uint32_t)cls, 0u, total}); total += cnt; }
+      }
+      if (total) {
+        CU(c->gseg.ensure(seg.size() * sizeof(GatherSeg)));
+        CU(cudaMemcpyAsync(c->gseg.p, seg.data(), seg.size() * sizeof(GatherSeg),
+                           cudaMemcpyHostToDevice, s));
+        CU(cudaEventRecord(c->ev[14], s));
+        CU(cudaStreamWaitEvent(c->gstream, c->ev[14], 0));
+        k_gather_arena<<<32, 1024, 0, c->gstream>>>(A, gather_src, const_cast<uint8_t *>(d_arena),
+                                                    (const GatherSeg *)c->gseg.p, (int)seg.size(),
+                                                    total, (uint32_t *)c->pready.p);
+        ++launches;
+        CU(cudaGetLastError());
+      }
+      CU(cudaEventRecord(arena_done, c->gstream));
+    }
   }
   // No host round trip before the kernels: the strip-boundary scratch is
   // sized for the longest supported sequence and the traceback pool is one
@@ -706,8 +750,24 @@ int align_range(int device, const uint8_t *arena, uint64_t arena_bytes, const sw
   if (!out_on_device) CU(c->out.ensure(n_pairs * sizeof(sw_result_t)));
   sw_result_t *d_out = out_on_device ? out : (sw_result_t *)c->out.p;
   cudaStream_t cs = c->copy_stream;
+  // A pinned (device-mapped) host arena is gathered by the device itself, in
+  // the order the packed pass consumes it (k_gather_arena): the forward of
+  // the first duos does not wait for bytes it does not need.  Otherwise the
+  // arena goes up by DMA in slices, each followed by a `ready` bump.
+  static const int env_gather = [] {
+    const char *e = getenv("PASTIS_SW_GATHER");
+    return e ? atoi(e) : 1;
+  }();
+  const uint8_t *gsrc = nullptr;
+  if (env_gather && span > 0) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, arena + lo) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer)
+      gsrc = (const uint8_t *)at.devicePointer - lo;
+    cudaGetLastError();
+  }
   const uint64_t slice = std::max<uint64_t>((uint64_t)4 << 20, (span + kMaxSlices - 1) / kMaxSlices);
-  const int nslices = (int)((span + slice - 1) / slice);
+  const int nslices = gsrc ? 0 : (int)((span + slice - 1) / slice);
   CU(cudaEventRecord(c->ev[8], s));
   CU(cudaStreamWaitEvent(cs, c->ev[8], 0));
   CU(cudaMemsetAsync(c->readyb.p, 0, 4, cs));
@@ -718,11 +778,11 @@ int align_range(int device, const uint8_t *arena, uint64_t arena_bytes, const sw
     CU(cudaMemcpyAsync((uint8_t *)c->arena.p + b0, arena + lo + b0, nb, cudaMemcpyHostToDevice, cs));
     CU(cudaMemcpyAsync(c->readyb.p, c->slice_vals + k, 4, cudaMemcpyHostToDevice, cs));
   }
-  CU(cudaEventRecord(c->ev_arena, cs));
+  if (!gsrc) CU(cudaEventRecord(c->ev_arena, cs));
   CU(cudaStreamWaitEvent(s, c->ev_pairs, 0));
   rc = run_device(c, (const uint8_t *)c->arena.p - lo, hi, (const sw_pair_t *)c->pairs.p, n_pairs,
                   params, d_out, s, tm, nslices > 0 ? (const uint32_t *)c->readyb.p : nullptr, slice,
-                  c->ev_arena, lo);
+                  c->ev_arena, lo, gsrc);
   if (rc) return rc;
   CU(cudaEventRecord(c->ev[10], s));
   if (!out_on_device)
@@ -736,7 +796,7 @@ int align_range(int device, const uint8_t *arena, uint64_t arena_bytes, const sw
             ev_ms(c->ev[0], c->ev[10]), ev_ms(c->ev[10], c->ev[11]), now_ms() - t0);
   }
   if (tm) {
-    tm->h2d_ms = ev_ms(c->ev[8], c->ev_arena);   // overlaps the forward pass
+    tm->h2d_ms = ev_ms(c->ev[8], c->ev_arena);   // overlaps the forward pass (gathered: incl. the wait)
     tm->d2h_ms = ev_ms(c->ev[10], c->ev[11]);
     tm->h2d_bytes = span + n_pairs * sizeof(sw_pair_t);
     tm->d2h_bytes = out_on_device ? 0 : n_pairs * sizeof(sw_result_t);

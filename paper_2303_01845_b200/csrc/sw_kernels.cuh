@@ -133,6 +133,9 @@ struct KArgs {
   // have landed (written by the copy stream); nullptr = arena fully resident
   const volatile uint32_t *ready;
   uint64_t slice_bytes;
+  // host arena gathered on the device (k_gather_arena): per-pair flags set
+  // once the pair's bytes are in the device arena; nullptr = not gathering
+  const volatile uint32_t *pair_ready;
   uint2 *cta_rows;         // K1cp: per-CTA ring of strip bottom rows (sw_cta_packed.cuh)
   int2 *bnd;               // per-warp strip boundary rows
   uint64_t bnd_stride;     // int2 per warp
@@ -208,6 +211,68 @@ __device__ __forceinline__ void wait_arena(const KArgs &A, uint64_t end, int lan
     while (*A.ready < need) __nanosleep(256);
   }
   __syncwarp();
+}
+
+// Wait until the gather kernel has copied pairs k0 (and k1 >= 0) into the
+// device arena (no-op when the arena is resident).
+__device__ __forceinline__ void wait_pairs(const KArgs &A, int64_t k0, int64_t k1, int lane) {
+  if (A.pair_ready == nullptr) return;
+  if (lane == 0) {
+    while (A.pair_ready[k0] == 0u) __nanosleep(200);
+    if (k1 >= 0)
+      while (A.pair_ready[k1] == 0u) __nanosleep(200);
+    __threadfence();
+  }
+  __syncwarp();
+}
+
+// Gather of a pinned host arena into the device arena in the order the packed
+// pass will consume it (segments: round r of the packed class lists -- list
+// positions [r cnt/Rn, (r+1) cnt/Rn) of every class -- then the long-pair
+// lists), one warp per pair: 128-bit loads over PCIe (zero-copy), byte
+// stores, then the pair's ready flag.  Pairs sharing a sequence copy the same
+// bytes twice (identical data).
+struct GatherSeg {
+  uint32_t list;    // stage * kNumClasses + cls
+  uint32_t j0;      // first list position of the segment
+  uint32_t start;   // global item index of the segment's first item
+};
+__device__ __forceinline__ void warp_copy16(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst,
+                                            uint32_t len, int lane) {
+  // src + i -> dst + i for i < len; loads aligned on the source's absolute
+  // address (the over-read stays inside the 16-byte words, hence the page)
+  if (len == 0) return;
+  const uintptr_t a0 = (uintptr_t)src, a1 = a0 + len;
+  for (uintptr_t w = (a0 & ~(uintptr_t)15) + 16u * lane; w < a1; w += 16u * 32) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(w));   // streamed: read once
+    const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      const uintptr_t pos = w + b;
+      if (pos >= a0 && pos < a1) dst[pos - a0] = (uint8_t)(x[b >> 2] >> (8 * (b & 3)));
+    }
+  }
+}
+__global__ void k_gather_arena(KArgs A, const uint8_t *__restrict__ src, uint8_t *dst,
+                               const GatherSeg *__restrict__ seg, int nseg, uint32_t total,
+                               uint32_t *ready) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += nw) {
+    int lo = 0, hi = nseg - 1;                 // last segment with start <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (seg[mid].start <= i) lo = mid; else hi = mid - 1;
+    }
+    const GatherSeg g = seg[lo];
+    const uint32_t k = A.lists[(uint64_t)g.list * A.n_pairs + g.j0 + (i - g.start)];
+    const sw_pair_t p = A.pairs[k];
+    warp_copy16(src + p.a_off, dst + p.a_off, p.a_len, lane);
+    warp_copy16(src + p.b_off, dst + p.b_off, p.b_len, lane);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicExch(&ready[k], 1u);
+  }
 }
 
 // Build this lane's slice of the query profile for rows row0+lane*R .. +R-1.

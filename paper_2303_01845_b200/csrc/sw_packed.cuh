@@ -243,8 +243,9 @@ k_score_packed(KArgs A, int stage, int cls) {
         arena_end = max(arena_end, max(p.a_off + p.a_len, p.b_off + p.b_len));
         P[h].m = (int)p.a_len;
         P[h].n = (int)p.b_len;
-        const uint8_t *seq = A.ready ? A.raw : A.codes;
-        const uint8_t *lut = A.ready ? A.lut : nullptr;
+        const bool raw = A.ready || A.pair_ready;   // host arena still arriving: raw bytes + LUT
+        const uint8_t *seq = raw ? A.raw : A.codes;
+        const uint8_t *lut = raw ? A.lut : nullptr;
         P[h].rows = RawView{seq + p.a_off, lut};
         P[h].cols = RawView{seq + p.b_off, lut};
       } else {
@@ -257,6 +258,7 @@ k_score_packed(KArgs A, int stage, int cls) {
       P[h].ck_off = 0;
     }
     wait_arena(A, arena_end, lane);   // host-pipelined arena: its slices may still be arriving
+    wait_pairs(A, P[0].k, P[1].k, lane);   // gathered arena: this duo's bytes
     const int m = max(P[0].m, P[1].m), n = max(P[0].n, P[1].n);
     const int nstrips = (m + 32 * R - 1) / (32 * R);
     const CkLayout CL = ck_layout(R, n);
