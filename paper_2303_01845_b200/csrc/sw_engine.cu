@@ -95,6 +95,7 @@ struct DeviceCtx {
   // gathered host arenas: per-pair ready flags, gather segments, their stream
   DevBuf pready, gseg;
   cudaStream_t gstream = nullptr;
+  cudaStream_t fstream = nullptr;   // the packed classes' forward passes, in class order (gathered arena)
   DevBuf skeys, svals, cubtmp;  // work-list sort
   DevBuf km_arena, km_off, km_len, km_base, km_keys, km_runs, km_pairs, km_out, km_small;
   cudaEvent_t ev[16];
@@ -227,6 +228,7 @@ int get_ctx(int device, DeviceCtx **out) {
     }
     CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithPriority(&c->gstream, cudaStreamNonBlocking, prio_greatest));
+    CU(cudaStreamCreateWithPriority(&c->fstream, cudaStreamNonBlocking, prio_least));
     CU(cudaEventCreateWithFlags(&c->ev_pairs, cudaEventDisableTiming));
     CU(cudaEventCreate(&c->ev_arena));
     CU(c->readyb.ensure(64));
@@ -442,19 +444,17 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     ++launches;
     CU(cudaGetLastError());
     if (gather_src) {
-      // gather order: kGatherRounds rounds through every packed class list
-      // (the classes run concurrently, each at its own pace through its
-      // list), then the long-pair lists (whose kernels wait for all of it)
-      constexpr int kGatherRounds = 64;
+      // gather order: the packed class lists, then the long-pair lists
+      // (whose kernels wait for all of it)
+      // the packed classes' forward passes run one after the other on one
+      // stream in this mode (below), so the gather follows their lists in
+      // that order
       std::vector<GatherSeg> seg;
       uint32_t total = 0;
-      for (int r = 0; r < kGatherRounds; ++r)
-        for (int cls = 0; cls < kNumClasses; ++cls) {
-          const uint32_t cnt = plan_cnt[6 * kNumClasses + cls];
-          const uint32_t j0 = (uint32_t)((uint64_t)cnt * r / kGatherRounds);
-          const uint32_t j1 = (uint32_t)((uint64_t)cnt * (r + 1) / kGatherRounds);
-          if (j1 > j0) { seg.push_back({(uint32_t)(6 * kNumClasses + cls), j0, total}); total += j1 - j0; }
-        }
+      for (int cls = 0; cls < kNumClasses; ++cls) {
+        const uint32_t cnt = plan_cnt[6 * kNumClasses + cls];
+        if (cnt) { seg.push_back({(uint32_t)(6 * kNumClasses + cls), 0u, total}); total += cnt; }
+      }
       for (int cls = 0; cls < kNumClasses; ++cls) {
         const uint32_t cnt = plan_cnt[cls];
         if (cnt) { seg.push_back({(uint32_t)cls, 0u, total}); total += cnt; }
@@ -526,6 +526,12 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     // short/medium pairs: packed forward + checkpoints, then the tile
     // traceback, one stream per length class
     CU(cudaEventRecord(c->ev_fork, s));
+    // The packed classes' persistent forward grids each fill the GPU, so they
+    // run nearly one after the other anyway; with a gathered arena they run
+    // strictly in class order on one stream (the order the gather follows),
+    // each class's tile traceback on its own stream behind it.
+    const bool serial_fwd = A.pair_ready != nullptr && pround == 0;
+    if (serial_fwd) CU(cudaStreamWaitEvent(c->fstream, c->ev_fork, 0));
     for (int cls = 0; cls < kNumClasses; ++cls) {
       cudaStream_t cs = c->cstream[cls];
       CU(cudaStreamWaitEvent(cs, c->ev_fork, 0));
@@ -536,8 +542,10 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
         CU(cudaEventRecord(c->ev_tb[cls], cs));
         continue;
       }
-      c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, cs>>>(A, 6, cls);
-      CU(cudaEventRecord(c->ev_k1[cls], cs));
+      cudaStream_t fs = serial_fwd ? c->fstream : cs;
+      c->ckpt[cls].fn<<<c->ckpt[cls].grid, kWarpsPerBlockP * 32, c->ckpt[cls].smem, fs>>>(A, 6, cls);
+      CU(cudaEventRecord(c->ev_k1[cls], fs));
+      if (fs != cs) CU(cudaStreamWaitEvent(cs, c->ev_k1[cls], 0));
       c->tb[cls].fn<<<c->tb[cls].grid, kTbWarps * 32, 0, cs>>>(A, 7, cls);
       CU(cudaEventRecord(c->ev_tb[cls], cs));
       launches += 2;
