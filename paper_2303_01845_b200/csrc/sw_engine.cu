@@ -465,7 +465,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
                            cudaMemcpyHostToDevice, s));
         CU(cudaEventRecord(c->ev[14], s));
         CU(cudaStreamWaitEvent(c->gstream, c->ev[14], 0));
-        k_gather_arena<<<32, 1024, 0, c->gstream>>>(A, gather_src, const_cast<uint8_t *>(d_arena),
+        static const int env_gb = [] {
+          const char *e = getenv("PASTIS_SW_GATHER_BLOCKS");
+          return e ? std::max(1, atoi(e)) : 32;
+        }();
+        k_gather_arena<<<env_gb, 1024, 0, c->gstream>>>(A, gather_src, const_cast<uint8_t *>(d_arena),
                                                     (const GatherSeg *)c->gseg.p, (int)seg.size(),
                                                     total, (uint32_t *)c->pready.p);
         ++launches;
@@ -530,7 +534,11 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
     // run nearly one after the other anyway; with a gathered arena they run
     // strictly in class order on one stream (the order the gather follows),
     // each class's tile traceback on its own stream behind it.
-    const bool serial_fwd = A.pair_ready != nullptr && pround == 0;
+    static const int env_serial = [] {
+      const char *e = getenv("PASTIS_SW_SERIAL_FWD");
+      return e ? atoi(e) : -1;
+    }();
+    const bool serial_fwd = pround == 0 && (env_serial >= 0 ? env_serial == 1 : A.pair_ready != nullptr);
     if (serial_fwd) CU(cudaStreamWaitEvent(c->fstream, c->ev_fork, 0));
     for (int cls = 0; cls < kNumClasses; ++cls) {
       cudaStream_t cs = c->cstream[cls];
