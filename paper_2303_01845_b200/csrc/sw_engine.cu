@@ -467,7 +467,7 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
         CU(cudaStreamWaitEvent(c->gstream, c->ev[14], 0));
         static const int env_gb = [] {
           const char *e = getenv("PASTIS_SW_GATHER_BLOCKS");
-          return e ? std::max(1, atoi(e)) : 32;
+          return e ? std::max(1, atoi(e)) : 16;
         }();
         k_gather_arena<<<env_gb, 1024, 0, c->gstream>>>(A, gather_src, const_cast<uint8_t *>(d_arena),
                                                     (const GatherSeg *)c->gseg.p, (int)seg.size(),
