@@ -134,31 +134,57 @@ class ResultList(Sequence):
     read, so a batch of 1M pairs costs no Python objects until the caller
     touches them (`records`, `ok` and `cells` give vectorised access)."""
 
-    __slots__ = ("records", "ok", "cells", "_n")
+    __slots__ = ("records", "_ok", "_cells", "_n", "_la", "_lb", "_index")
 
     def __init__(self, batch: PackedBatch, rec: np.ndarray):
         n = self._n = batch.n_input
-        ok = rec["status"] == _native.STATUS_OK
-        cells = batch.pairs["a_len"].astype(np.int64) * batch.pairs["b_len"]
-        if len(batch.index) == n:          # no packing errors: packed order == input order
-            self.records, self.ok, self.cells = rec, ok, cells
+        # the pair lengths are kept (not the pinned table they came in):
+        # ok / cells are derived on first use
+        self._la = np.array(batch.pairs["a_len"])
+        self._lb = np.array(batch.pairs["b_len"])
+        self._index = None if len(batch.index) == n else batch.index
+        if self._index is None:            # no packing errors: packed order == input order
+            self.records = rec
         else:
             self.records = np.zeros(n, dtype=_native.RESULT_DTYPE)
-            self.records[batch.index] = rec
-            self.ok = np.zeros(n, dtype=bool)
-            self.ok[batch.index] = ok
-            self.cells = np.zeros(n, dtype=np.int64)
-            self.cells[batch.index] = cells
+            self.records[self._index] = rec
+        self._ok = self._cells = None
+
+    @property
+    def ok(self) -> np.ndarray:
+        if self._ok is None:
+            ok = self.records["status"] == _native.STATUS_OK
+            if self._index is not None:
+                present = np.zeros(self._n, dtype=bool)
+                present[self._index] = True
+                ok &= present
+            self._ok = ok
+        return self._ok
+
+    @property
+    def cells(self) -> np.ndarray:
+        if self._cells is None:
+            c = self._la.astype(np.int64) * self._lb
+            if self._index is not None:
+                full = np.zeros(self._n, dtype=np.int64)
+                full[self._index] = c
+                c = full
+            self._cells = c
+        return self._cells
 
     def __len__(self) -> int:
         return self._n
 
     def _make(self, i: int):
-        if not self.ok[i]:
-            return None
         r = self.records[i]
+        if r[7] != _native.STATUS_OK or (self._index is not None and not self.ok[i]):
+            return None
+        if self._index is None:
+            c = int(self._la[i]) * int(self._lb[i])
+        else:
+            c = int(self.cells[i])
         return AlignmentResult(int(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4]), int(r[5]),
-                               int(r[6]), int(self.cells[i]))
+                               int(r[6]), c)
 
     def __getitem__(self, i):
         if isinstance(i, slice):
@@ -201,9 +227,10 @@ def _to_results(batch: PackedBatch, rec: np.ndarray):
             errors.append((idx, AssertionError("traceback lost at H state")))
     if len(bad):
         errors.sort(key=lambda e: e[0])
-    ok = results.ok
     if not len(bad) and len(batch.index) == batch.n_input:
-        return results, errors, batch.n_input, int(results.cells.sum())
+        cells = int(np.dot(batch.pairs["a_len"].astype(np.uint64), batch.pairs["b_len"].astype(np.uint64)))
+        return results, errors, batch.n_input, cells
+    ok = results.ok
     return results, errors, int(ok.sum()), int(results.cells[ok].sum())
 
 
@@ -270,7 +297,7 @@ def _align(pairs: Sequence[tuple], params: AlignParams, devices, gpu_lock=None) 
         return b.array
 
     try:
-        batch = pack_pairs(pairs, alloc=alloc)
+        batch = pack_pairs(pairs, alloc=alloc, table_alloc=alloc)
         t1 = perf_counter()
         if gpu_lock is None:
             rec, timings = align_packed(batch, params, devices)

@@ -61,13 +61,18 @@ def _numpy_alloc(nbytes: int) -> np.ndarray:
     return np.empty(nbytes, dtype=np.uint8)
 
 
-def pack_pairs(pairs, alloc=None) -> PackedBatch:
+def pack_pairs(pairs, alloc=None, table_alloc=None) -> PackedBatch:
     """Pack (a, b[, payload]) items; invalid pairs are reported, not packed.
 
     `alloc(nbytes)` returns the writable arena buffer (default: a new numpy
-    array); it is called once, after the table is known."""
+    array); it is called once, after the table is known.  `table_alloc(nbytes)`
+    likewise supplies the pair table's buffer (the engine passes pinned memory
+    for both)."""
     n = len(pairs)
-    table = np.empty(n, dtype=PAIR_DTYPE)
+    if table_alloc is not None and n:
+        table = np.asarray(table_alloc(n * PAIR_DTYPE.itemsize)).view(PAIR_DTYPE)[:n]
+    else:
+        table = np.empty(n, dtype=PAIR_DTYPE)
     index = np.empty(n, dtype=np.int64)
     holder = {}
 

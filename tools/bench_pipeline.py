@@ -43,6 +43,7 @@ def cpu_align_baseline(fa_path, td):
                           "--pairs-file", path, "--gap-open", "11", "--gap-extend", "2"],
                          cwd=ROOT, capture_output=True, text=True, check=True)
     r = json.loads(out.stdout.strip().splitlines()[-1])
+    r["workload"] = "the pipeline's SW pairs"
     r["note"] = ("numpy restatement of align.py:79-181 (the reference algorithm) over the "
                  "pipeline's SW pairs, forked lanes on the host cores")
     return r
