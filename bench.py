@@ -437,7 +437,8 @@ def main():
                 tms.append(tm)
                 launches += tm["launches"]
         barrier()
-    dev_ms = float(np.sum(max_over_ranks(step_ms)))
+    step_max = max_over_ranks(step_ms)
+    dev_ms = float(np.sum(step_max))
     total_cells = cells_all * args.steps
     value = total_cells / (dev_ms / 1e3) / 1e9
     rec_dev = (gathered.cpu().numpy().view(_native.RESULT_DTYPE).reshape(-1)[:n_all]
@@ -527,6 +528,7 @@ def main():
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": dev_ms / args.steps,
+        "step_ms_max_over_ranks": [round(x, 3) for x in step_max],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,

@@ -1213,7 +1213,10 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
 }
 
 template <int R>
-__global__ void __launch_bounds__(kTbWarps * 32, (R >= 8 ? 7 : 6))
+#ifndef K5_MINB9
+#define K5_MINB9 7
+#endif
+__global__ void __launch_bounds__(kTbWarps * 32, (R == 9 ? K5_MINB9 : R >= 8 ? 7 : 6))
 k_tb(KArgs A, int stage, int cls) {
   struct Shared {
     TbSmem<R> t[kTbWarps];
