@@ -625,7 +625,12 @@ def api_leg(args, arena_np, table_np, cells, flush, torch) -> dict:
            "entry": "AlignEngine(lanes=1, use_processes=True).submit(list[(str, str, None)])"
                     ".result()"}
     if phases and phases[0]:
-        out["phase_ms"] = {k: float(np.mean([p[k] for p in phases])) * 1e3 for k in phases[0]}
+        out["phase_ms"] = {k: float(np.mean([p[k] for p in phases])) * 1e3 for k in phases[0]
+                           if k != "chunks"}
+        out["chunks"] = phases[0].get("chunks")
+        out["phase_note"] = ("pack = host packing not hidden behind the GPU (chunk k+1 packs "
+                             "while chunk k aligns), align = GPU calls, results = lazy "
+                             "result list + counters")
     return out
 
 

@@ -284,10 +284,11 @@ except ImportError:  # pragma: no cover
             self.kernel_seconds += other.kernel_seconds
 
 
-def _align(pairs: Sequence[tuple], params: AlignParams, devices, gpu_lock=None) -> tuple:
-    """pack (host, C threads) -> align (GPU; under gpu_lock when given, so a
-    second in-flight batch packs while this one runs) -> lazy results."""
-    t0 = perf_counter()
+_CHUNK = 1 << 18     # pairs per pipelined chunk of a large API batch
+
+
+def _pack(pairs):
+    """pack_pairs into recycled pinned buffers; returns (batch, buffers)."""
     pool = _native.pinned_pool()
     bufs = []
 
@@ -297,24 +298,84 @@ def _align(pairs: Sequence[tuple], params: AlignParams, devices, gpu_lock=None) 
         return b.array
 
     try:
-        batch = pack_pairs(pairs, alloc=alloc, table_alloc=alloc)
-        t1 = perf_counter()
-        if gpu_lock is None:
-            rec, timings = align_packed(batch, params, devices)
-        else:
-            with gpu_lock:
-                t1 = perf_counter()
-                rec, timings = align_packed(batch, params, devices)
-    finally:
+        return pack_pairs(pairs, alloc=alloc, table_alloc=alloc), bufs
+    except BaseException:
         for b in bufs:
             b.release()
+        raise
+
+
+class _Lengths:
+    """What _to_results needs of a batch once its pinned buffers are gone."""
+
+    def __init__(self, la, lb, index, n_input, errors):
+        self.pairs = np.empty(len(la), dtype=[("a_len", "<u4"), ("b_len", "<u4")])
+        self.pairs["a_len"], self.pairs["b_len"] = la, lb
+        self.index, self.n_input, self.errors = index, n_input, errors
+
+
+def _align(pairs: Sequence[tuple], params: AlignParams, devices, gpu_lock=None) -> tuple:
+    """pack (host, C threads) -> align (GPU; under gpu_lock when given, so a
+    second in-flight batch packs while this one runs) -> lazy results.
+
+    A large batch is cut into chunks of _CHUNK pairs and pipelined: a helper
+    thread packs chunk k+1 (the C extension releases the GIL while copying)
+    while the GPU aligns chunk k; results, errors and counters come back as
+    for one batch, in input order."""
+    from contextlib import nullcontext
+    lock = gpu_lock if gpu_lock is not None else nullcontext()
+    n = len(pairs)
+    t0 = perf_counter()
+    bounds = [(0, n)] if n <= 2 * _CHUNK else [(c, min(n, c + _CHUNK)) for c in range(0, n, _CHUNK)]
+    pieces, timings = [], []
+    t_pack = t_align = 0.0
+    ex = ThreadPoolExecutor(max_workers=1, thread_name_prefix="pastis-pack") if len(bounds) > 1 else None
+    try:
+        fut = None
+        tp = perf_counter()
+        nxt = _pack(pairs if len(bounds) == 1 else pairs[bounds[0][0]:bounds[0][1]])
+        t_pack += perf_counter() - tp
+        for k, (c0, c1) in enumerate(bounds):
+            batch, bufs = nxt
+            if k + 1 < len(bounds):
+                d0, d1 = bounds[k + 1]
+                fut = ex.submit(_pack, pairs[d0:d1])
+            try:
+                with lock:
+                    ta = perf_counter()
+                    rec, tms = align_packed(batch, params, devices)
+                    t_align += perf_counter() - ta
+                timings += tms
+                # keep what the results need before the pinned buffers go back
+                pieces.append((rec, np.array(batch.pairs["a_len"]), np.array(batch.pairs["b_len"]),
+                               batch.index + c0, [(i + c0, e) for i, e in batch.errors]))
+            finally:
+                for b in bufs:
+                    b.release()
+            if fut is not None:
+                tp = perf_counter()
+                nxt = fut.result()
+                t_pack += perf_counter() - tp    # only the part not hidden behind the GPU
+                fut = None
+    finally:
+        if ex is not None:
+            ex.shutdown(wait=True)
     t2 = perf_counter()
-    results, errors, n_ok, cell_sum = _to_results(batch, rec)
+    if len(pieces) == 1:
+        rec, la, lb, index, errs = pieces[0]
+    else:
+        rec = np.concatenate([p[0] for p in pieces])
+        la = np.concatenate([p[1] for p in pieces])
+        lb = np.concatenate([p[2] for p in pieces])
+        index = np.concatenate([p[3] for p in pieces])
+        errs = [e for p in pieces for e in p[4]]
+    results, errors, n_ok, cell_sum = _to_results(_Lengths(la, lb, index, n, errs), rec)
     t3 = perf_counter()
     # kernel_seconds = forward fill time, the quantity align.py:103-122 times
     fwd = sum(t["forward_ms"] for t in timings) / 1e3
     counters = BatchCounters(alignments=n_ok, cells=cell_sum, kernel_seconds=fwd)
-    phases = {"pack": t1 - t0, "align": t2 - t1, "results": t3 - t2}
+    phases = {"pack": t_pack, "align": t_align, "results": t3 - t2, "chunks": len(bounds),
+              "total": t3 - t0}
     return results, errors, counters, timings, phases
 
 

@@ -203,3 +203,36 @@ def test_interop_with_reference_classes_when_importable():
             "print('ok')\n")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
+
+
+def test_chunked_pipeline_merges_like_one_batch(monkeypatch):
+    """AlignEngine's large-batch pipeline (pack chunk k+1 while chunk k is on
+    the GPU) returns the same results, errors and counters as one batch.  The
+    device call is replaced by the C oracle here (CPU test of the host logic)."""
+    from oracle import oracle
+    from paper_2303_01845_b200 import _native
+    from paper_2303_01845_b200 import align as A
+    mat = matrix("blosum62")
+
+    def fake_align_packed(batch, params, devices=(0,)):
+        ref = oracle.align_batch_c(batch.arena, batch.pairs, params.gap_open, params.gap_extend,
+                                   mat, threads=4)
+        rec = np.zeros(len(batch.pairs), dtype=_native.RESULT_DTYPE)
+        for k, f in enumerate(FIELDS):
+            rec[f] = ref[:, k]
+        return rec, [{"forward_ms": 1.0}]
+
+    monkeypatch.setattr(A, "align_packed", fake_align_packed)
+    rng = np.random.default_rng(7)
+    letters = list("ACDEFGHIKLMNPQRSTVWY")
+    seqs = ["".join(rng.choice(letters, size=int(n))) for n in rng.integers(5, 60, size=80)]
+    pairs = [(seqs[k % 80], seqs[(k * 3 + 1) % 80] if k % 41 else "", k) for k in range(700)]
+    params = sw.AlignParams(gap_open=11, gap_extend=1)
+    one = A._align(pairs, params, [0])
+    monkeypatch.setattr(A, "_CHUNK", 64)
+    many = A._align(pairs, params, [0])
+    assert many[4]["chunks"] == 11
+    assert [e[0] for e in one[1]] == [e[0] for e in many[1]]
+    assert one[2].alignments == many[2].alignments and one[2].cells == many[2].cells
+    assert list(one[0]) == list(many[0])
+    assert many[0][41] is None and many[0][3].cells == len(seqs[3]) * len(seqs[10])
