@@ -748,15 +748,25 @@ int align_range(int device, const uint8_t *arena, uint64_t arena_bytes, const sw
   // the byte range the pairs reference (pairs outside the arena are left to
   // the device check: the range is clamped to the arena)
   uint64_t lo = 0, hi = arena_bytes;
-  if (!whole) {
-    lo = ~0ull;
-    hi = 0;
-    for (uint64_t k = k0; k < k1; ++k) {
-      const sw_pair_t &p = pairs[k];
-      lo = std::min(lo, std::min(p.a_off, p.b_off));
-      hi = std::max(hi, std::max(p.a_off + p.a_len, p.b_off + p.b_len));
-    }
-    hi = std::min(hi, arena_bytes);
+  if (!whole) {   // a few threads for large ranges (one pass over the range's table)
+    const int T = (int)std::max<uint64_t>(1, std::min<uint64_t>(8, n_pairs / 131072));
+    std::vector<uint64_t> tlo(T, ~0ull), thi(T, 0);
+    auto scan = [&](int t) {
+      uint64_t l = ~0ull, h = 0;
+      for (uint64_t k = k0 + n_pairs * t / T, e = k0 + n_pairs * (t + 1) / T; k < e; ++k) {
+        const sw_pair_t &p = pairs[k];
+        l = std::min(l, std::min(p.a_off, p.b_off));
+        h = std::max(h, std::max(p.a_off + p.a_len, p.b_off + p.b_len));
+      }
+      tlo[t] = l;
+      thi[t] = h;
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(scan, t);
+    scan(0);
+    for (auto &x : th) x.join();
+    lo = *std::min_element(tlo.begin(), tlo.end());
+    hi = std::min(*std::max_element(thi.begin(), thi.end()), arena_bytes);
     lo = std::min(lo, hi);
   }
   cudaStream_t s = user_stream ? user_stream : c->stream;
