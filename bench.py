@@ -259,6 +259,21 @@ def ncu_fields(workload: str, per_step_ms: float) -> dict:
     return out
 
 
+def hbm_view(alg_bytes: int, cells: int, fwd_ms: float) -> dict:
+    """The same forward phase against the HBM roofline (MEASURED_PEAKS.json):
+    algorithmic bytes (residues + pair entries + results) per second -- a tiny
+    fraction, i.e. HBM is not what bounds the kernel (the int-issue roofline
+    above is)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak, src = float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        peak, src = 6650.0, "fallback (B200_PROFILING.md)"
+    ach = alg_bytes / (fwd_ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": src, "basis": "algorithmic bytes of the batch / forward-phase time"}
+
+
 # --- reference arm ----------------------------------------------------------
 def run_reference(args, rank: int, world: int) -> None:
     """--impl reference: the reference algorithm on the host cores (rank 0 only),
@@ -570,6 +585,7 @@ def main():
                      "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 56/(m*n) "
                                  f"= {(arena_np.size + 56 * n_all) / cells_all:.4f} B -> non-binding",
                      "alu_pipe_ceiling": sms * clk_ghz * 4 * 64 / 11.0,
+                     "hbm_view": hbm_view(arena_np.size + 56 * n_all, cells_all, fwd_ms),
                      **cc,
                      **ncu_fields(args.workload, dev_ms / args.steps)},
         "e2e": {"value": e2e_value, "unit": "GCUPS",
