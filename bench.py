@@ -585,7 +585,7 @@ def main():
                      "hbm_note": "algorithmic bytes/cell = (m+n)/(m*n) + 56/(m*n) "
                                  f"= {(arena_np.size + 56 * n_all) / cells_all:.4f} B -> non-binding",
                      "alu_pipe_ceiling": sms * clk_ghz * 4 * 64 / 11.0,
-                     "hbm_view": hbm_view(arena_np.size + 56 * n_all, cells_all, fwd_ms),
+                     "hbm_view": hbm_view((arena_np.size + 56 * n_all) * (n_local / n_all), cells_all, fwd_ms),
                      **cc,
                      **ncu_fields(args.workload, dev_ms / args.steps)},
         "e2e": {"value": e2e_value, "unit": "GCUPS",
