@@ -21,17 +21,19 @@
 // checkpoints (k_tb).  Values are exact while every biased value stays below
 // 65535 - 128; a warp that gets near that re-runs both pairs in the wide path.
 #pragma once
-#include <type_traits>
 #include "sw_kernels.cuh"
 
 namespace pastis {
 
 constexpr int kWarpsPerBlockP = 4;
+#ifndef K1P_UNROLL
+#define K1P_UNROLL 8
+#endif
+constexpr int kUnrollP = K1P_UNROLL;   // wavefront steps per unrolled chunk
 #ifndef K1P_PROF_UNROLL
 #define K1P_PROF_UNROLL 7
 #endif
 constexpr int kProfUnroll = K1P_PROF_UNROLL;   // code groups per profile-build iteration
-constexpr int kStageBytesP = 17 * 8 * 8;         // (16 boundaries + dummy) x 8 steps x (Ho2, F2)
 constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs
 constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
 constexpr int32_t kTileMax = 32767;               // largest score k_tb's int16 tiles hold
@@ -51,7 +53,7 @@ __host__ __device__ constexpr int prof_p1(int R) {
 }
 __host__ __device__ constexpr int prof_bytes_p(int R) { return kCodes * 32 * (prof_p0(R) + prof_p1(R)); }
 __host__ __device__ constexpr int warp_bytes_p(int R) {
-  return (2 * prof_bytes_p(R) + kStageBytesP + kRingBytes + 15) / 16 * 16;
+  return (2 * prof_bytes_p(R) + kRingBytes + 15) / 16 * 16;
 }
 __host__ __device__ constexpr int smem_packed(int R) { return kMatTBytes + kWarpsPerBlockP * warp_bytes_p(R); }
 // resident blocks per SM the packed forward is compiled for (registers):
@@ -215,8 +217,7 @@ k_score_packed(KArgs A, int stage, int cls) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t *profA = smem + kMatTBytes + warp * warp_bytes_p(R);
   uint8_t *profB = profA + prof_bytes_p(R);
-  uint2 *rstage = reinterpret_cast<uint2 *>(profB + prof_bytes_p(R));   // [17][8] (Ho2, F2)
-  uint8_t *ringA = reinterpret_cast<uint8_t *>(rstage + 17 * 8);
+  uint8_t *ringA = profB + prof_bytes_p(R);
   uint8_t *ringB = ringA + 128;
   load_matrix_t(smatT, A.mat, A.prof_lo);
   const uint32_t Bs = (uint32_t)A.bias16;
@@ -326,47 +327,55 @@ k_score_packed(KArgs A, int stage, int cls) {
         ringA[c & 127] = (c >= 0 && c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
         ringB[c & 127] = (c >= 0 && c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
       }
-      // the per-step "row above from the previous strip" branch is compiled
-      // out of the first strip (the common, single-strip case)
-      auto run_strip = [&](auto above_tag) {
-        constexpr bool has_above = decltype(above_tag)::value;
+      // the next refill's codes (columns 96 + lane), loaded one refill ahead
+      // (A/B on the box: forward +1.2 % config 3, +0.9 % config 2)
+      uint8_t nxtA = 96 + lane < P[0].n ? (uint8_t)P[0].cols.at(96 + lane) : (uint8_t)kPad;
+      uint8_t nxtB = 96 + lane < P[1].n ? (uint8_t)P[1].cols.at(96 + lane) : (uint8_t)kPad;
+      // Row above the strip (lane 0): the previous strip's bottom row; strip 0
+      // gets an empty reader, which returns the zero row.  One loop for every
+      // strip: a second copy without the reader for strip 0 was 3.4 % slower
+      // on config 3 (instruction-cache misses: "no instruction" stalls 0.35
+      // per issue with two copies of the 8-step loop) and 1.6 % faster on
+      // config 2.
       PackedBoundaryReader br;
       const uint2 dflt = make_uint2(HO0, NEG2);   // (H-open at H=0, F=-inf), both halves
-      if (has_above)
-        br.init(rowck + ((uint64_t)(strip - 1) * CL.row_words + (uint64_t)(CL.nb - 1) * 2 * CL.spad) / 2,
-                n, lane, dflt);
+      br.init(rowck + ((uint64_t)max(strip - 1, 0) * CL.row_words + (uint64_t)(CL.nb - 1) * 2 * CL.spad) / 2,
+              strip > 0 ? n : 0, lane, dflt);
       // checkpoint destinations for this strip
       uint32_t *colA = P[0].ck + (uint64_t)strip * CL.col_words + lane;
       uint32_t *colB = P[1].ck ? P[1].ck + (uint64_t)strip * CL.col_words + lane : nullptr;
       const int b = ck_boundary(lane, CL);
-      const int bslot = (b >= 0 ? b : 16) * kScoreUnroll;   // non-boundary lanes -> dummy row
-      // row checkpoints of this strip, [boundary][step] uint2 = 16 B per two
-      // steps: lane i (and i + 32) flush 16 B chunk i of the staged 8 steps
+      // row checkpoints of this strip, [boundary][step] uint2
       uint4 *rowdst = reinterpret_cast<uint4 *>(rowck + (uint64_t)strip * CL.row_words / 2);
-      const int nchunk = CL.nb * 4;
       const int steps = n + 31;
+      // boundary lanes keep their bottom rows of 8 steps in registers and
+      // write them as four 16-B stores (64 contiguous bytes of [boundary][step]);
+      // A/B on the box against staging through shared memory and a warp-wide
+      // flush: forward +4.5 % (config 3), +5.7 % (config 2)
+      uint4 *rowmine = b >= 0 ? rowdst + (uint64_t)b * (CL.spad / 2) : nullptr;
+      uint2 rowv[kUnrollP];
       __syncwarp();
-      for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
+      for (int s0 = 0; s0 < steps; s0 += kUnrollP) {
         if ((s0 & 31) == 0 && s0 > 0) {    // refill ring slots for columns s0+64 .. s0+95
           const int c = s0 + 64 + lane;
-          ringA[c & 127] = (c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
-          ringB[c & 127] = (c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
+          ringA[c & 127] = nxtA;
+          ringB[c & 127] = nxtB;
+          nxtA = c + 32 < P[0].n ? (uint8_t)P[0].cols.at(c + 32) : (uint8_t)kPad;
+          nxtB = c + 32 < P[1].n ? (uint8_t)P[1].cols.at(c + 32) : (uint8_t)kPad;
           __syncwarp();
         }
 #pragma unroll
-        for (int q = 0; q < kScoreUnroll; ++q) {
+        for (int q = 0; q < kUnrollP; ++q) {
           const int s = s0 + q;
           const int c = s - lane;
           const uint4 pa = load_profile_u8<R>(profA, ringA[c & 127], lane);
           const uint4 pb = load_profile_u8<R>(profB, ringB[c & 127], lane);
           uint32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
           uint32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
-          if (has_above) {
+          {
             uint32_t bho, bf;
             br.get(s, lane, dflt, bho, bf);
             if (lane == 0) { upHo = bho; upF = bf; }
-          } else if (lane == 0) {
-            upHo = HO0; upF = NEG2;
           }
           uint32_t diag = L.hoUpPrev;
           L.hoUpPrev = upHo;
@@ -408,16 +417,16 @@ k_score_packed(KArgs A, int stage, int cls) {
 #endif
           L.botHo = L.Ho[R - 1];
           L.botF = G - OPEN2;
-          rstage[bslot + q] = make_uint2(L.botHo, L.botF);
+          rowv[q] = make_uint2(L.botHo, L.botF);
         }
-        __syncwarp();
-        for (int i = lane; i < nchunk; i += 32)   // chunk i: boundary i / 4, steps 2(i % 4) ..
-          rowdst[(uint64_t)(i >> 2) * (CL.spad / 2) + s0 / 2 + (i & 3)] =
-              reinterpret_cast<const uint4 *>(rstage)[i];
-        __syncwarp();
+        if (rowmine) {
+#pragma unroll
+          for (int i = 0; i < kUnrollP / 2; ++i)
+            rowmine[s0 / 2 + i] = make_uint4(rowv[2 * i].x, rowv[2 * i].y, rowv[2 * i + 1].x, rowv[2 * i + 1].y);
+        }
         // column checkpoint: state entering window w (after step 32w - 1)
-        if (((s0 + kScoreUnroll) & 31) == 0) {
-          const int w = (s0 + kScoreUnroll) >> 5;
+        if (((s0 + kUnrollP) & 31) == 0) {
+          const int w = (s0 + kUnrollP) >> 5;
           if (w < CL.nwin) {
             const uint64_t base = (uint64_t)w * 32 * (2 * R + 1);
             {
@@ -439,9 +448,6 @@ k_score_packed(KArgs A, int stage, int cls) {
           }
         }
       }
-      };
-      if (strip > 0) run_strip(std::true_type{});
-      else run_strip(std::false_type{});
       // strip reduction: best and the first row reaching it, per pair
 #pragma unroll
       for (int r = 0; r < R; ++r) {
