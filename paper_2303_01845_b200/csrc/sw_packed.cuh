@@ -64,8 +64,13 @@ __host__ __device__ constexpr int smem_packed(int R) { return kMatTBytes + kWarp
 #ifndef K1P_MINB_MID
 #define K1P_MINB_MID 4
 #endif
+#ifndef K1P_R4MAX
+#define K1P_R4MAX 8
+#endif
 __host__ __device__ constexpr int packed_min_blocks(int R) {
-  return R <= 4 ? K1P_MINB_SMALL : R <= 6 ? K1P_MINB_MID : 3;
+  // R = 7, 8: 128 registers and 55 KB of shared memory, 4 blocks per SM
+  // (A/B on the box against 3: forward +1.5 % on config 3)
+  return R <= 4 ? K1P_MINB_SMALL : R <= 6 ? K1P_MINB_MID : R <= K1P_R4MAX ? 4 : 3;
 }
 
 __device__ __forceinline__ uint32_t vmax2u(uint32_t a, uint32_t b) {
