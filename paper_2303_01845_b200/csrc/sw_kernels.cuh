@@ -327,14 +327,18 @@ struct BoundaryReader {
 // traceback can replay only the 32-column tiles its path crosses:
 //  * column checkpoints: at the end of every 32-step window w-1 each lane
 //    stores its state entering window w: (Ho_r, E_r) for its R rows,
-//    (hoUpPrev, F_bot), and the running row maxima -> 2R+1 words, values
-//    as biased u16 (v + B);
+//    (hoUpPrev, F_bot), and the running maximum over its R rows -> R+2
+//    words, values as biased u16 (v + B) (per-row maxima: 2R+1 words, ~1 %
+//    slower forward on configs 2/3 for the rare second j_end tile they save);
 //  * row checkpoints: "boundary" lanes (the last lane of each group of
 //    G = 32/R lanes, and lane 31) store their bottom-row (Ho, F) every step.
-// Per strip: [window][word 0..2R][lane] words per pair (coalesced stores), and
+// Per strip: [window][word 0..R+1][lane] words per pair (coalesced stores), and
 // [boundary][step][2] words per duo -- the raw (Ho2, F2) u16x2 words of the
 // packed pass, both pairs in one word (PairState.row_delta, kFlagHi).
 // ---------------------------------------------------------------------------
+// column-checkpoint words per lane and window: (Ho, E) of each of the R rows,
+// (hoUpPrev, F_bot), and the running maximum over the lane's rows
+__host__ __device__ constexpr int ck_words(int R) { return R + 2; }
 struct CkLayout {
   int G, nb, nwin, spad;
   uint32_t col_words;   // per pair and strip: column checkpoints
@@ -346,7 +350,7 @@ __host__ __device__ inline CkLayout ck_layout(int R, int n) {
   L.nb = (32 + L.G - 1) / L.G;
   L.nwin = (n + 31 + 31) / 32;
   L.spad = L.nwin * 32;
-  L.col_words = (uint32_t)L.nwin * 32u * (uint32_t)(2 * R + 1);
+  L.col_words = (uint32_t)L.nwin * 32u * (uint32_t)ck_words(R);
   L.row_words = 2u * (uint32_t)L.nb * (uint32_t)L.spad;
   return L;
 }
@@ -920,7 +924,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   uint32_t ckx = 0u, cky = 0u;
   const bool have_ck = (w > 0) & row_ok;
   if (have_ck) {
-    const uint32_t *wd = sbase + (uint64_t)w * 32 * (2 * R + 1) + tq;
+    const uint32_t *wd = sbase + (uint64_t)w * 32 * ck_words(R) + tq;
     ckx = wd[32 * rq];
     cky = wd[32 * R];
   }
@@ -983,7 +987,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   {
     auto pf = [](const void *ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); };
     if (w > 1 && row_ok) {
-      const uint32_t *wd = sbase + (uint64_t)(w - 1) * 32 * (2 * R + 1) + tq;
+      const uint32_t *wd = sbase + (uint64_t)(w - 1) * 32 * ck_words(R) + tq;
       pf(wd + 32 * rq);
       if (rq == 0) pf(wd + 32 * R);
     }
@@ -991,7 +995,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       const int g2 = g - 1, t2 = g2 * CL.G;
       const int qq = lane, tqq = t2 + qq / R, rqq = qq - (qq / R) * R;
       if (qq < CL.G * R) {
-        const uint32_t *wd = sbase + (uint64_t)w * 32 * (2 * R + 1) + tqq;
+        const uint32_t *wd = sbase + (uint64_t)w * 32 * ck_words(R) + tqq;
         pf(wd + 32 * rqq);
         if (rqq == 0) pf(wd + 32 * R);
       }
@@ -1087,32 +1091,38 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
   int cs = -1, cg = -1, cw = -1, trow0 = 0, tcmin = 0, tqmax = -1;
   if (st->flags & kFlagNeedJ) {
     // The packed forward pass knows best and i_end only.  j_end = first
-    // column of row i_end with H == best: the per-window running row maxima
-    // in the checkpoints give its window w*; replaying that tile gives the
-    // column (align.py:124 row-major-first end cell).
+    // column of row i_end with H == best (align.py:124).  The checkpoints
+    // hold, per window, the running maximum over the R rows of each lane: the
+    // first window where the lane of row i_end reaches best is the earliest
+    // row i_end can; the tiles of row i_end are replayed from there until the
+    // row reaches best (a second replay only when a later row of the same
+    // lane reached best first).
     const int best = st->best;
     const int strip = i_end / (32 * R);
-    const int t = (i_end - strip * 32 * R) / R, r = i_end - strip * 32 * R - t * R;
-    const uint32_t *rmcol = ck + (uint64_t)strip * CL.col_words + 32ull * (R + 1 + r) + t;
+    const int t = (i_end - strip * 32 * R) / R;
+    const uint32_t *lmcol = ck + (uint64_t)strip * CL.col_words + 32ull * (R + 1) + t;
     int wstar = CL.nwin - 1;
     for (int w0 = 1; w0 < CL.nwin; w0 += 32) {
       const int w = w0 + lane;
       bool hit = false;
-      if (w < CL.nwin) hit = (int32_t)(rmcol[(uint64_t)w * 32 * (2 * R + 1)] & 0xFFFFu) - Bias >= best;
+      if (w < CL.nwin) hit = (int32_t)(lmcol[(uint64_t)w * 32 * ck_words(R)] & 0xFFFFu) - Bias >= best;
       const uint32_t hm = __ballot_sync(0xffffffffu, hit);
       if (hm) { wstar = w0 + __ffs(hm) - 1 - 1; break; }
     }
     const int g = t / CL.G;
-    const int kap_hi = min(32 * wstar - t + 31, n - 1);
-    tb_replay<R>(T, smat, slut, ck, rowck, hi, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
-                 EXT, Bias, trow0, tcmin, i_end, kap_hi);
-    cs = strip; cg = g; cw = wstar;
-    const int q = i_end - trow0;
-    tqmax = q;
-    const int c = 32 * wstar - t + lane;
-    const bool hit = (c >= 0) && (c <= kap_hi) && ((int32_t)T.H[q + 1][c - tcmin + 1] >= best);
-    const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-    j_end = hm ? 32 * wstar - t + __ffs(hm) - 1 : -1;
+    for (; wstar < CL.nwin; ++wstar) {
+      const int kap_hi = min(32 * wstar - t + 31, n - 1);
+      if (32 * wstar - t > kap_hi) continue;
+      tb_replay<R>(T, smat, slut, ck, rowck, hi, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
+                   EXT, Bias, trow0, tcmin, i_end, kap_hi);
+      cs = strip; cg = g; cw = wstar;
+      const int q = i_end - trow0;
+      tqmax = q;
+      const int c = 32 * wstar - t + lane;
+      const bool hit = (c >= 0) && (c <= kap_hi) && ((int32_t)T.H[q + 1][c - tcmin + 1] >= best);
+      const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+      if (hm) { j_end = 32 * wstar - t + __ffs(hm) - 1; break; }
+    }
   }
   int i = i_end + 1, j = j_end + 1, state = 0, matches = 0, aln = 0;
   bool lost = j_end < 0;

@@ -362,22 +362,23 @@ k_score_packed(KArgs A, int stage, int cls) {
       // column checkpoint: state entering window w (after step 32w - 1)
       auto colck = [&](int w) {
         if (w < CL.nwin) {
-          const uint64_t base = (uint64_t)w * 32 * (2 * R + 1);
+          const uint64_t base = (uint64_t)w * 32 * ck_words(R);
+          uint32_t lm = L.rm[0];   // running maximum over the lane's rows (k_tb's j_end search)
+#pragma unroll
+          for (int r = 1; r < R; ++r) lm = vmax2u(lm, L.rm[r]);
           {
             uint32_t *d = colA + base;
 #pragma unroll
             for (int r = 0; r < R; ++r) d[32 * r] = prmt(L.Ho[r], L.E[r], 0x5410u);
             d[32 * R] = prmt(L.hoUpPrev, L.botF, 0x5410u);
-#pragma unroll
-            for (int r = 0; r < R; ++r) d[32 * (R + 1 + r)] = L.rm[r] & 0xFFFFu;
+            d[32 * (R + 1)] = lm & 0xFFFFu;
           }
           if (colB) {
             uint32_t *d = colB + base;
 #pragma unroll
             for (int r = 0; r < R; ++r) d[32 * r] = prmt(L.Ho[r], L.E[r], 0x7632u);
             d[32 * R] = prmt(L.hoUpPrev, L.botF, 0x7632u);
-#pragma unroll
-            for (int r = 0; r < R; ++r) d[32 * (R + 1 + r)] = L.rm[r] >> 16;
+            d[32 * (R + 1)] = lm >> 16;
           }
         }
       };
