@@ -1031,9 +1031,8 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   int32_t prevHb = 0, prevFb = kNeg16;   // H / F of the previous row at ITS c_lo - 1
   const int32_t Kl = (lane + 1) * EXT - OPEN, lext = lane * EXT;
   __syncwarp();
-  int qq = 0;
-  for (int tb = t0; qq <= qmax; ++tb) {     // forward lanes of the tile
-    if (qq > 0) {                           // columns shift left by one: row above one lane up
+  for (int tb = t0, qs = 0; qs <= qmax; ++tb, qs += R) {   // forward lanes of the tile
+    if (qs > 0) {                           // columns shift left by one: row above one lane up
       const int32_t sh = __shfl_up_sync(0xffffffffu, upH, 1);
       const int32_t sf = __shfl_up_sync(0xffffffffu, upF, 1);
       upH = lane == 0 ? prevHb : sh;
@@ -1041,9 +1040,11 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
     }
     const int xs = (t1 - tb) + 1 + lane;    // tile column of this lane's cell
     const int8_t *mcol = smat + T.bcode[xs - 1];
+    const int nr = min(R, qmax + 1 - qs);   // rows of this forward lane to replay
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if (qq > qmax) break;
+      if (r >= nr) break;
+      const int qq = qs + r;
       const int4 rw = T.row[qq];             // broadcast
       int32_t dg = __shfl_up_sync(0xffffffffu, upH, 1);
       if (lane == 0) dg = r == 0 ? rw.w : prevHb;
@@ -1065,7 +1066,6 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       upF = f;
       prevHb = rw.y;
       prevFb = rw.w;                         // used after the forward lane's last row
-      ++qq;
     }
   }
   __syncwarp();

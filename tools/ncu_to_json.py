@@ -40,7 +40,9 @@ def launch_shares(path):
                 v *= {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(unit, 1)
                 agg[name][0] += 1
                 agg[name][1] += v
-    tot = sum(v[1] for v in agg.values())
+    # the e2e leg's device gather of pinned host arenas moves bytes over PCIe
+    # (serialised under ncu): reported, but not part of the step's kernel shares
+    tot = sum(v[1] for k, v in agg.items() if "k_gather_arena" not in k)
     out = {}
     for name in sorted(agg, key=lambda k: -agg[k][1]):
         n, t = agg[name]
@@ -49,6 +51,8 @@ def launch_shares(path):
         out[name] = {"launches": n, "total_ms": round(t / 1e6, 3), "share": round(t / tot, 4)}
     groups = defaultdict(float)
     for name, v in out.items():
+        if "k_gather_arena" in name:
+            continue
         key = ("K1p k_score_packed" if "k_score_packed" in name else
                "K5 k_tb" if "k_tb" in name else
                "K1cp k_score_cta_packed" if "k_score_cta_packed" in name else "other")
