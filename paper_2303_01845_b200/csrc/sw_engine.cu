@@ -365,9 +365,12 @@ int run_device(DeviceCtx *c, const uint8_t *d_arena, uint64_t arena_bytes,
   // gathered host arena: the pair's bytes are pulled over PCIe by
   // k_gather_arena in consumption order; K1p waits per duo on its flags
   if (gather_src) {
-    CU(c->pready.ensure(n_pairs * 4));
-    CU(cudaMemsetAsync(c->pready.p, 0, n_pairs * 4, s));
+    CU(c->pready.ensure(n_pairs * 4 + 4));
+    CU(cudaMemsetAsync(c->pready.p, 0, n_pairs * 4 + 4, s));
     A.pair_ready = (const uint32_t *)c->pready.p;
+    A.gather_count = (const uint32_t *)c->pready.p + n_pairs;
+    A.gather_src = gather_src;
+    A.gather_dst = const_cast<uint8_t *>(d_arena);
   }
   A.cta_rows = (uint2 *)c->cta_rows.p;
   A.open_ = prm->gap_open;

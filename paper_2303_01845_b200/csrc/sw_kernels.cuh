@@ -136,6 +136,9 @@ struct KArgs {
   // host arena gathered on the device (k_gather_arena): per-pair flags set
   // once the pair's bytes are in the device arena; nullptr = not gathering
   const volatile uint32_t *pair_ready;
+  const uint8_t *gather_src;   // the pinned host arena (device-mapped) being gathered
+  uint8_t *gather_dst;         // the device arena it is gathered into (same offsets)
+  const volatile uint32_t *gather_count;   // pairs the gather kernel has copied so far
   uint2 *cta_rows;         // K1cp: per-CTA ring of strip bottom rows (sw_cta_packed.cuh)
   int2 *bnd;               // per-warp strip boundary rows
   uint64_t bnd_stride;     // int2 per warp
@@ -213,19 +216,6 @@ __device__ __forceinline__ void wait_arena(const KArgs &A, uint64_t end, int lan
   __syncwarp();
 }
 
-// Wait until the gather kernel has copied pairs k0 (and k1 >= 0) into the
-// device arena (no-op when the arena is resident).
-__device__ __forceinline__ void wait_pairs(const KArgs &A, int64_t k0, int64_t k1, int lane) {
-  if (A.pair_ready == nullptr) return;
-  if (lane == 0) {
-    while (A.pair_ready[k0] == 0u) __nanosleep(200);
-    if (k1 >= 0)
-      while (A.pair_ready[k1] == 0u) __nanosleep(200);
-    __threadfence();
-  }
-  __syncwarp();
-}
-
 // Gather of a pinned host arena into the device arena in the order the packed
 // pass will consume it (segments: round r of the packed class lists -- list
 // positions [r cnt/Rn, (r+1) cnt/Rn) of every class -- then the long-pair
@@ -253,6 +243,53 @@ __device__ __forceinline__ void warp_copy16(const uint8_t *__restrict__ src, uin
     }
   }
 }
+// Wait until the gather kernel has copied pairs k0 (and k1 >= 0) into the
+// device arena (no-op when the arena is resident).  The gather kernel runs
+// beside the packed pass and is normally far ahead; if a pair is not ready
+// while the gather makes no progress for 20 us -- e.g. the packed pass's
+// blocks hold every SM and the gather kernel's blocks never became resident --
+// the warp copies the pair itself (identical bytes; the gather may copy it
+// again), so no schedule can deadlock.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void wait_pairs(const KArgs &A, int64_t k0, int64_t k1, int lane) {
+  if (A.pair_ready == nullptr) return;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    const int64_t k = h ? k1 : k0;
+    if (k < 0) continue;
+    int ok = 0;
+    if (lane == 0) {
+      // give up only when the gather has made no progress for 20 us
+      uint64_t t0 = globaltimer_ns();
+      uint32_t seen = *A.gather_count;
+      while (!(ok = A.pair_ready[k] != 0u)) {
+        __nanosleep(200);
+        if (globaltimer_ns() - t0 > 20000ull) {
+          const uint32_t now = *A.gather_count;
+          if (now == seen) break;
+          seen = now;
+          t0 = globaltimer_ns();
+        }
+      }
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) {
+      const sw_pair_t p = A.pairs[k];
+      warp_copy16(A.gather_src + p.a_off, A.gather_dst + p.a_off, p.a_len, lane);
+      warp_copy16(A.gather_src + p.b_off, A.gather_dst + p.b_off, p.b_len, lane);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicExch(const_cast<uint32_t *>(A.pair_ready + k), 1u);
+    }
+  }
+  if (lane == 0) __threadfence();
+  __syncwarp();
+}
+
 __global__ void k_gather_arena(KArgs A, const uint8_t *__restrict__ src, uint8_t *dst,
                                const GatherSeg *__restrict__ seg, int nseg, uint32_t total,
                                uint32_t *ready) {
@@ -271,7 +308,10 @@ __global__ void k_gather_arena(KArgs A, const uint8_t *__restrict__ src, uint8_t
     warp_copy16(src + p.b_off, dst + p.b_off, p.b_len, lane);
     __threadfence();
     __syncwarp();
-    if (lane == 0) atomicExch(&ready[k], 1u);
+    if (lane == 0) {
+      atomicExch(&ready[k], 1u);
+      atomicAdd(const_cast<uint32_t *>(A.gather_count), 1u);
+    }
   }
 }
 

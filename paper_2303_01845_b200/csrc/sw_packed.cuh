@@ -34,7 +34,10 @@ constexpr int kUnrollP = K1P_UNROLL;   // wavefront steps per unrolled chunk
 #define K1P_PROF_UNROLL 7
 #endif
 constexpr int kProfUnroll = K1P_PROF_UNROLL;   // code groups per profile-build iteration
-constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs
+constexpr int kRingBytes = 2 * 128;              // column-code rings of the two pairs (K1cp)
+// K1p's rings: 128 slots + a mirror of slots 0..7, so the 8 steps of a chunk
+// read slots base + q without wrapping
+constexpr int kRingSlot = 136;
 constexpr int kBndBytes = 32 * 8;                 // K1p: the row above, 32 columns of (Ho2, F2)
 constexpr uint32_t kPackedLimit = 65535u - 160u;  // overflow guard on biased values
 constexpr int32_t kTileMax = 32767;               // largest score k_tb's int16 tiles hold
@@ -54,7 +57,7 @@ __host__ __device__ constexpr int prof_p1(int R) {
 }
 __host__ __device__ constexpr int prof_bytes_p(int R) { return kCodes * 32 * (prof_p0(R) + prof_p1(R)); }
 __host__ __device__ constexpr int warp_bytes_p(int R) {
-  return (2 * prof_bytes_p(R) + kRingBytes + kBndBytes + 15) / 16 * 16;
+  return (2 * prof_bytes_p(R) + 2 * kRingSlot + kBndBytes + 15) / 16 * 16;
 }
 __host__ __device__ constexpr int smem_packed(int R) { return kMatTBytes + kWarpsPerBlockP * warp_bytes_p(R); }
 // resident blocks per SM the packed forward is compiled for (registers):
@@ -216,7 +219,7 @@ k_score_packed(KArgs A, int stage, int cls) {
   uint8_t *profA = smem + kMatTBytes + warp * warp_bytes_p(R);
   uint8_t *profB = profA + prof_bytes_p(R);
   uint8_t *ringA = profB + prof_bytes_p(R);
-  uint8_t *ringB = ringA + 128;
+  uint8_t *ringB = ringA + kRingSlot;
   load_matrix_t(smatT, A.mat, A.prof_lo);
   const uint32_t Bs = (uint32_t)A.bias16;
   const uint32_t BB = A.p_bb;
@@ -322,8 +325,11 @@ k_score_packed(KArgs A, int stage, int cls) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = -32 + 32 * q + lane;
-        ringA[c & 127] = (c >= 0 && c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
-        ringB[c & 127] = (c >= 0 && c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
+        const uint8_t va = (c >= 0 && c < P[0].n) ? (uint8_t)P[0].cols.at(c) : (uint8_t)kPad;
+        const uint8_t vb = (c >= 0 && c < P[1].n) ? (uint8_t)P[1].cols.at(c) : (uint8_t)kPad;
+        ringA[c & 127] = va;
+        ringB[c & 127] = vb;
+        if ((c & 127) < 8) { ringA[(c & 127) + 128] = va; ringB[(c & 127) + 128] = vb; }
       }
       // the next refill's codes (columns 96 + lane), loaded one refill ahead
       // (A/B on the box: forward +1.2 % config 3, +0.9 % config 2)
@@ -378,7 +384,7 @@ k_score_packed(KArgs A, int stage, int cls) {
       // lane 0 reads the row above from shared memory: 32 columns staged at
       // each refill, one broadcast LDS per step instead of two shuffles (A/B
       // on the box: forward +2.3 % config 3, +0.8 % config 2)
-      uint2 *bnd = reinterpret_cast<uint2 *>(ringB + 128);
+      uint2 *bnd = reinterpret_cast<uint2 *>(ringB + kRingSlot);
       bnd[lane] = br.cur;
       __syncwarp();
       for (int s0 = 0; s0 < steps; s0 += kUnrollP) {
@@ -390,18 +396,19 @@ k_score_packed(KArgs A, int stage, int cls) {
           const int c = s0 + 64 + lane;
           ringA[c & 127] = nxtA;
           ringB[c & 127] = nxtB;
+          if ((c & 127) < 8) { ringA[(c & 127) + 128] = nxtA; ringB[(c & 127) + 128] = nxtB; }
           nxtA = c + 32 < P[0].n ? (uint8_t)P[0].cols.at(c + 32) : (uint8_t)kPad;
           nxtB = c + 32 < P[1].n ? (uint8_t)P[1].cols.at(c + 32) : (uint8_t)kPad;
           bnd[lane] = br.nxt;
           br.nxt = br.ld(s0 + 32 + lane, dflt);
           __syncwarp();
         }
+        const int rbase = (s0 - lane) & 127;   // ring slot of this lane's column at step s0
 #pragma unroll
         for (int q = 0; q < kUnrollP; ++q) {
           const int s = s0 + q;
-          const int c = s - lane;
-          const uint4 pa = load_profile_u8<R>(profA, ringA[c & 127], lane);
-          const uint4 pb = load_profile_u8<R>(profB, ringB[c & 127], lane);
+          const uint4 pa = load_profile_u8<R>(profA, ringA[rbase + q], lane);
+          const uint4 pb = load_profile_u8<R>(profB, ringB[rbase + q], lane);
           uint32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
           uint32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
           {

@@ -313,6 +313,41 @@ def test_pipelined_host_upload_matches_resident_arena():
     assert (got == ref[:, :7]).all()
 
 
+def test_gathered_arena_without_gather_progress_is_exact():
+    """A pinned host arena is gathered to the device by k_gather_arena while
+    the packed pass consumes it; a packed warp whose pair has not arrived
+    within 20 us copies it itself, so the call completes even when the gather
+    kernel gets no SM.  With one gather block (PASTIS_SW_GATHER_BLOCKS=1) most
+    pairs take that path: results equal the resident-arena path."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+from paper_2303_01845_b200 import _native, blosum62
+from paper_2303_01845_b200.batch import pack_codes
+from pastis_synth import workloads
+sa, sb = workloads.config3_bulk(40_000, seed=9)
+arena, table = pack_codes(sa, sb)
+p = _native.make_params(11, 1, np.asarray(blosum62.MATRIX, dtype=np.int32))
+ref, _ = _native.align_host(arena, table, p)
+buf = _native.pinned_pool().acquire(arena.size)
+buf.array[:] = arena
+got, _ = _native.align_host(buf.array, table, p)
+buf.release()
+print(json.dumps({"bad": int((got != ref).sum()), "ok": int((got["status"] == 0).sum()), "n": len(table)}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PASTIS_SW_GATHER_BLOCKS="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["bad"] == 0 and res["ok"] == res["n"], res
+
+
 def test_reverse_box_path_for_every_pair_exact():
     """PASTIS_SW_TRACEBACK=box sends every pair through the anchored reverse
     pass (with its dead-strip early stop) + box traceback: still exact on the
