@@ -38,7 +38,7 @@ struct CtaPSync {
 };
 
 __host__ __device__ constexpr int cta_packed_warp_bytes(int R) {
-  return 2 * prof_bytes_p(R) + kRingBytes;
+  return 2 * prof_bytes_p(R) + 2 * kRingSlot + kBndBytes;   // profiles, mirrored rings, row above
 }
 __host__ __device__ constexpr int smem_cta_packed(int R) {
   return kMatTBytes + kCtaWarps * cta_packed_warp_bytes(R) + (int)sizeof(CtaPSync) + 16;
@@ -53,7 +53,8 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
   uint8_t *profA = smem + kMatTBytes + warp * cta_packed_warp_bytes(R);
   uint8_t *profB = profA + prof_bytes_p(R);
   uint8_t *ringA = profB + prof_bytes_p(R);
-  uint8_t *ringB = ringA + 128;
+  uint8_t *ringB = ringA + kRingSlot;
+  uint2 *bnd = reinterpret_cast<uint2 *>(ringB + kRingSlot);   // 32 columns of the row above
   CtaPSync &S = *reinterpret_cast<CtaPSync *>(smem + kMatTBytes + kCtaWarps * cta_packed_warp_bytes(R));
   load_matrix_t(smatT, A.mat, A.prof_lo);
   uint2 *rows_ring = A.cta_rows + (uint64_t)blockIdx.x * kCtaPSlots * kCtaPRowStride;
@@ -114,8 +115,11 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = -32 + 32 * q + lane;
-        ringA[c & 127] = (c >= 0 && c < n0) ? (uint8_t)cols0.at(c) : (uint8_t)kPad;
-        ringB[c & 127] = (c >= 0 && c < n1) ? (uint8_t)cols1.at(c) : (uint8_t)kPad;
+        const uint8_t va = (c >= 0 && c < n0) ? (uint8_t)cols0.at(c) : (uint8_t)kPad;
+        const uint8_t vb = (c >= 0 && c < n1) ? (uint8_t)cols1.at(c) : (uint8_t)kPad;
+        ringA[c & 127] = va;
+        ringB[c & 127] = vb;
+        if ((c & 127) < 8) { ringA[(c & 127) + 128] = va; ringB[(c & 127) + 128] = vb; }
       }
       int nxtA = 96 + lane < n0 ? cols0.at(96 + lane) : kPad;   // next refill, loaded ahead
       int nxtB = 96 + lane < n1 ? cols1.at(96 + lane) : kPad;
@@ -144,6 +148,7 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
             const int c = s0 + 64 + lane;
             ringA[c & 127] = (uint8_t)nxtA;
             ringB[c & 127] = (uint8_t)nxtB;
+            if ((c & 127) < 8) { ringA[(c & 127) + 128] = (uint8_t)nxtA; ringB[(c & 127) + 128] = (uint8_t)nxtB; }
             nxtA = c + 32 < n0 ? cols0.at(c + 32) : kPad;
             nxtB = c + 32 < n1 ? cols1.at(c + 32) : kPad;
           }
@@ -160,18 +165,22 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
             }
           }
           __syncwarp();
+          bnd[lane] = cur;   // lane 0 reads column s from shared memory (one LDS, no shuffles)
+          __syncwarp();
         }
+        const int rbase = (s0 - lane) & 127;   // ring slot of this lane's column at step s0
+        uint2 rowv[kScoreUnroll];
 #pragma unroll
         for (int q = 0; q < kScoreUnroll; ++q) {
           const int s = s0 + q;
-          const int c = s - lane;
-          const uint4 pa = load_profile_u8<R>(profA, ringA[c & 127], lane);
-          const uint4 pb = load_profile_u8<R>(profB, ringB[c & 127], lane);
+          const uint4 pa = load_profile_u8<R>(profA, ringA[rbase + q], lane);
+          const uint4 pb = load_profile_u8<R>(profB, ringB[rbase + q], lane);
           uint32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
           uint32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
-          const uint32_t tHo = __shfl_sync(0xffffffffu, cur.x, s & 31);
-          const uint32_t tF = __shfl_sync(0xffffffffu, cur.y, s & 31);
-          if (lane == 0) { upHo = tHo; upF = tF; }
+          {
+            const uint2 tv = bnd[s & 31];
+            if (lane == 0) { upHo = tv.x; upF = tv.y; }
+          }
           uint32_t diag = L.hoUpPrev;
           L.hoUpPrev = upHo;
           uint32_t G = upF + OPEN2, tprev = upHo + OPEN2;   // G = F + open (sw_packed.cuh)
@@ -189,9 +198,13 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
           }
           L.botHo = L.Ho[R - 1];
           L.botF = G - OPEN2;
-          if (has_below && lane == 31) {
-            const int cb = s - 31;
-            if (cb >= 0 && cb < n) out_row[cb] = make_uint2(L.botHo, L.botF);
+          rowv[q] = make_uint2(L.botHo, L.botF);
+        }
+        if (has_below && lane == 31) {   // the chunk's bottom row, columns s0-31 .. s0-24
+#pragma unroll
+          for (int q = 0; q < kScoreUnroll; ++q) {
+            const int cb = s0 + q - 31;
+            if (cb >= 0 && cb < n) out_row[cb] = rowv[q];
           }
         }
         if (has_below) {
