@@ -122,7 +122,9 @@ def align_packed(batch: PackedBatch, params: AlignParams, devices=(0,)):
     if len(batch.pairs) == 0:
         return np.empty(0, dtype=_native.RESULT_DTYPE), []
     if len(devices) == 1:
-        rec, tm = _native.align_host(batch.arena, batch.pairs, p, device=devices[0])
+        out = _native.pinned_array(len(batch.pairs) * _native.RESULT_DTYPE.itemsize)
+        rec, tm = _native.align_host(batch.arena, batch.pairs, p, device=devices[0],
+                                     out=out.view(_native.RESULT_DTYPE))
         return rec, [tm]
     return _native.align_multi(batch.arena, batch.pairs, p, devices)
 
@@ -140,8 +142,10 @@ class ResultList(Sequence):
         n = self._n = batch.n_input
         # the pair lengths are kept (not the pinned table they came in):
         # ok / cells are derived on first use
-        self._la = np.array(batch.pairs["a_len"])
-        self._lb = np.array(batch.pairs["b_len"])
+        # contiguous copies, detached from a (pinned) pair table; no copy
+        # when the caller already detached them (_Lengths)
+        self._la = np.ascontiguousarray(batch.pairs["a_len"])
+        self._lb = np.ascontiguousarray(batch.pairs["b_len"])
         self._index = None if len(batch.index) == n else batch.index
         if self._index is None:            # no packing errors: packed order == input order
             self.records = rec
@@ -228,7 +232,11 @@ def _to_results(batch: PackedBatch, rec: np.ndarray):
     if len(bad):
         errors.sort(key=lambda e: e[0])
     if not len(bad) and len(batch.index) == batch.n_input:
-        cells = int(np.dot(batch.pairs["a_len"].astype(np.uint64), batch.pairs["b_len"].astype(np.uint64)))
+        # float64 dot: exact while the sum stays below 2^53 (recomputed in
+        # integers otherwise)
+        cells = np.dot(results._la.astype(np.float64), results._lb.astype(np.float64))
+        cells = int(cells) if cells < 2.0 ** 52 else int(
+            np.dot(results._la.astype(np.uint64), results._lb.astype(np.uint64)))
         return results, errors, batch.n_input, cells
     ok = results.ok
     return results, errors, int(ok.sum()), int(results.cells[ok].sum())
@@ -310,11 +318,11 @@ def _pack(pairs):
 
 
 class _Lengths:
-    """What _to_results needs of a batch once its pinned buffers are gone."""
+    """What _to_results needs of a batch once its pinned buffers are gone
+    (the pair lengths as contiguous arrays, already copied out)."""
 
     def __init__(self, la, lb, index, n_input, errors):
-        self.pairs = np.empty(len(la), dtype=[("a_len", "<u4"), ("b_len", "<u4")])
-        self.pairs["a_len"], self.pairs["b_len"] = la, lb
+        self.pairs = {"a_len": la, "b_len": lb}
         self.index, self.n_input, self.errors = index, n_input, errors
 
 

@@ -31,6 +31,15 @@
 #include <pthread.h>
 #include <stdint.h>
 #include <string.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <time.h>
+
+static double now_ms(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
 
 #define MAX_RESIDUES 65000u
 #define CHUNK 4096
@@ -80,6 +89,40 @@ static uint64_t omap_get(omap_t *M, uintptr_t s, uint64_t pid) {
   }
 }
 
+/* Maps are kept between calls (a fresh 64 MB calloc costs its page faults
+ * on every call) and cleared by the worker threads after use; a small pool,
+ * since two batches may be packed concurrently (AlignEngine's two threads). */
+#define MAP_POOL 4
+static pthread_mutex_t map_mu = PTHREAD_MUTEX_INITIALIZER;
+static slot_t *map_free[MAP_POOL];
+static size_t map_cap[MAP_POOL];
+
+static slot_t *map_get(size_t cap) {
+  pthread_mutex_lock(&map_mu);
+  for (int i = 0; i < MAP_POOL; ++i)
+    if (map_free[i] && map_cap[i] == cap) {
+      slot_t *m = map_free[i];
+      map_free[i] = NULL;
+      pthread_mutex_unlock(&map_mu);
+      return m;
+    }
+  pthread_mutex_unlock(&map_mu);
+  return (slot_t *)calloc(cap, sizeof(slot_t));
+}
+
+static void map_put(slot_t *m, size_t cap) {   /* m must be all-zero */
+  pthread_mutex_lock(&map_mu);
+  for (int i = 0; i < MAP_POOL; ++i)
+    if (!map_free[i]) {
+      map_free[i] = m;
+      map_cap[i] = cap;
+      pthread_mutex_unlock(&map_mu);
+      return;
+    }
+  pthread_mutex_unlock(&map_mu);
+  free(m);
+}
+
 typedef struct {
   PyObject **items;
   Py_ssize_t n;
@@ -90,6 +133,12 @@ typedef struct {
   Py_ssize_t next;
   pthread_mutex_t mu;
   uint8_t *arena;              /* phase C destination */
+  size_t map_cap;              /* phase C also clears the map */
+  size_t clear_next;
+  int map_cleared;
+  uint64_t *blk;               /* prefix sum: per-block totals, then offsets */
+  Py_ssize_t nblk;
+  int prefix_write;
 } job_t;
 
 static inline int fast_str(PyObject *s) {
@@ -107,6 +156,24 @@ static void *phase_a(void *arg) {
     if (k0 >= J->n) break;
     const Py_ssize_t k1 = k0 + CHUNK < J->n ? k0 + CHUNK : J->n;
     for (Py_ssize_t k = k0; k < k1; ++k) {
+      /* software prefetch, three items deep per level: the tuple 12 ahead,
+       * its two str objects 6 ahead, their map slots 3 ahead (each item
+       * touches ~4 cold cache lines) */
+      if (k + 12 < k1) __builtin_prefetch(J->items[k + 12]);
+      if (k + 6 < k1) {
+        PyObject *t = J->items[k + 6];
+        if (PyTuple_CheckExact(t) && PyTuple_GET_SIZE(t) >= 2) {
+          __builtin_prefetch(PyTuple_GET_ITEM(t, 0));
+          __builtin_prefetch(PyTuple_GET_ITEM(t, 1));
+        }
+      }
+      if (k + 3 < k1) {
+        PyObject *t = J->items[k + 3];
+        if (PyTuple_CheckExact(t) && PyTuple_GET_SIZE(t) >= 2) {
+          __builtin_prefetch(&J->M->slot[hash_ptr((uintptr_t)PyTuple_GET_ITEM(t, 0)) & J->M->mask]);
+          __builtin_prefetch(&J->M->slot[hash_ptr((uintptr_t)PyTuple_GET_ITEM(t, 1)) & J->M->mask]);
+        }
+      }
       PyObject *item = J->items[k];
       J->pc[2 * k].len = 0;
       J->pc[2 * k + 1].len = 0;
@@ -130,6 +197,16 @@ static void *phase_a(void *arg) {
 
 static void *phase_c(void *arg) {
   job_t *J = (job_t *)arg;
+  /* clear the map for its next use, 1/threads of it per call of this function */
+  for (;;) {
+    pthread_mutex_lock(&J->mu);
+    const size_t s0 = J->clear_next;
+    J->clear_next += 1u << 16;
+    pthread_mutex_unlock(&J->mu);
+    if (s0 >= J->map_cap) break;
+    const size_t s1 = s0 + (1u << 16) < J->map_cap ? s0 + (1u << 16) : J->map_cap;
+    memset(J->M->slot + s0, 0, (s1 - s0) * sizeof(slot_t));
+  }
   const Py_ssize_t np = 2 * J->n;
   for (;;) {
     pthread_mutex_lock(&J->mu);
@@ -140,6 +217,33 @@ static void *phase_c(void *arg) {
     const Py_ssize_t k1 = k0 + 2 * CHUNK < np ? k0 + 2 * CHUNK : np;
     for (Py_ssize_t k = k0; k < k1; ++k)
       if (J->pc[k].len) memcpy(J->arena + J->pc[k].dst, J->pc[k].src, J->pc[k].len);
+  }
+  return NULL;
+}
+
+#define PREFIX_BLK 65536
+/* pass 1 (prefix_write 0): blk[b] = total length of block b's pieces;
+ * pass 2: dst of every piece = blk[b] (the block's offset) + running sum */
+static void *prefix_sum_pass(void *arg) {
+  job_t *J = (job_t *)arg;
+  for (;;) {
+    pthread_mutex_lock(&J->mu);
+    const Py_ssize_t b = J->next;
+    J->next += 1;
+    pthread_mutex_unlock(&J->mu);
+    if (b >= J->nblk) break;
+    const Py_ssize_t q0 = b * PREFIX_BLK, q1 = q0 + PREFIX_BLK < 2 * J->n ? q0 + PREFIX_BLK : 2 * J->n;
+    if (!J->prefix_write) {
+      uint64_t s = 0;
+      for (Py_ssize_t q = q0; q < q1; ++q) s += J->pc[q].len;
+      J->blk[b] = s;
+    } else {
+      uint64_t o = J->blk[b];
+      for (Py_ssize_t q = q0; q < q1; ++q) {
+        J->pc[q].dst = o;
+        o += J->pc[q].len;
+      }
+    }
   }
   return NULL;
 }
@@ -284,9 +388,11 @@ static PyObject *pack(PyObject *self, PyObject *args) {
     PyErr_SetString(PyExc_ValueError, "table/index buffers too small");
     goto out;
   }
+  const double t_0 = now_ms();
   size_t cap = 64;
   while (cap < (size_t)n * 4 + 16) cap <<= 1;
-  M.slot = (slot_t *)PyMem_Calloc(cap, sizeof(slot_t));
+  M.slot = map_get(cap);
+  J.map_cap = cap;
   M.mask = cap - 1;
   J.items = PySequence_Fast_ITEMS(seq);
   J.n = n;
@@ -295,19 +401,36 @@ static PyObject *pack(PyObject *self, PyObject *args) {
   J.state = (uint8_t *)PyMem_Malloc((size_t)n + 1);
   J.pc = (piece_t *)PyMem_Malloc(((size_t)n * 2 + 1) * sizeof(piece_t));
   if (!M.slot || !J.state || !J.pc) { PyErr_NoMemory(); goto out; }
+  const double t_alloc = now_ms();
   /* phase A: no Python calls; the GIL stays with this thread throughout */
   run_threads(phase_a, &J, n >= 2 * CHUNK ? threads : 1);
+  const double t_a = now_ms();
   /* phase B */
   for (Py_ssize_t k = 0; k < n; ++k)
     if (J.state[k] && slow_item(&J, k, keep, errors, err_cls) < 0) goto out;
-  /* arena offsets: prefix sum over the pieces in input order */
+  /* arena offsets: prefix sum over the pieces in input order (two threaded
+   * passes over blocks of pieces: block sums, then offsets) */
   uint64_t off = 0;
-  for (Py_ssize_t q = 0; q < 2 * n; ++q) {
-    J.pc[q].dst = off;
-    off += J.pc[q].len;
+  {
+    const Py_ssize_t np = 2 * n, nblk = (np + PREFIX_BLK - 1) / PREFIX_BLK;
+    J.blk = (uint64_t *)PyMem_Malloc(((size_t)nblk + 1) * sizeof(uint64_t));
+    if (!J.blk) { PyErr_NoMemory(); goto out; }
+    J.nblk = nblk;
+    run_threads(prefix_sum_pass, &J, nblk >= 8 ? threads : 1);
+    for (Py_ssize_t b = 0; b < nblk; ++b) {
+      const uint64_t t = J.blk[b];
+      J.blk[b] = off;
+      off += t;
+    }
+    J.prefix_write = 1;
+    run_threads(prefix_sum_pass, &J, nblk >= 8 ? threads : 1);
+    PyMem_Free(J.blk);
+    J.blk = NULL;
   }
+  const double t_b = now_ms();
   /* phase D: piece ids -> offsets */
   run_threads(phase_d, &J, n >= 2 * CHUNK ? threads : 1);
+  const double t_d = now_ms();
   /* compaction (only when some pair failed) */
   int64_t *index = (int64_t *)ib.buf;
   pair_t *table = (pair_t *)tb.buf;
@@ -336,16 +459,25 @@ static PyObject *pack(PyObject *self, PyObject *args) {
     }
     J.arena = (uint8_t *)ab.buf;
     const int tc = off >= (1u << 20) ? threads : 1;
+    const double t_c0 = now_ms();
+    J.clear_next = 0;
     Py_BEGIN_ALLOW_THREADS
     run_threads(phase_c, &J, tc);
     Py_END_ALLOW_THREADS
+    J.map_cleared = 1;
+    if (getenv("PASTIS_PACK_DEBUG"))
+      fprintf(stderr, "pack: n=%zd threads=%d alloc=%.2f A=%.2f B+prefix=%.2f D=%.2f arena_alloc=%.2f C=%.2f ms\n",
+              n, threads, t_alloc - t_0, t_a - t_alloc, t_b - t_a, t_d - t_b, t_c0 - t_d, now_ms() - t_c0);
     PyBuffer_Release(&ab);
     result = Py_BuildValue("(nOKO)", kept, arena_obj, (unsigned long long)off, errors);
   }
 out:
   pthread_mutex_destroy(&J.mu);
   Py_XDECREF(arena_obj);
-  PyMem_Free(M.slot);
+  if (M.slot) {
+    if (!J.map_cleared) memset(M.slot, 0, J.map_cap * sizeof(slot_t));
+    map_put(M.slot, J.map_cap);
+  }
   PyMem_Free(J.state);
   PyMem_Free(J.pc);
   Py_XDECREF(errors);
