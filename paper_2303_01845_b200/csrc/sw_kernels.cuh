@@ -1021,35 +1021,8 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
     T.H[0][t1 - t0 + 1 + lane] = (int16_t)(tHo + OPEN);
     topv = ((uint32_t)tHo & 0xFFFFu) | ((uint32_t)tF << 16);
   }
-  // The walk leaves this tile to the left (window w-1) or upwards (group
-  // g-1): prefetch those tiles' checkpoint lines into L2 now, so their replay
-  // does not start with a DRAM round trip.
-  {
-    auto pf = [](const void *ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); };
-    if (w > 1 && row_ok) {
-      const uint32_t *wd = sbase + (uint64_t)(w - 1) * 32 * ck_words(R) + tq;
-      pf(wd + 32 * rq);
-      if (rq == 0) pf(wd + 32 * R);
-    }
-    if (t0 > 0 && w > 0) {
-      const int g2 = g - 1, t2 = g2 * CL.G;
-      const int qq = lane, tqq = t2 + qq / R, rqq = qq - (qq / R) * R;
-      if (qq < CL.G * R) {
-        const uint32_t *wd = sbase + (uint64_t)w * 32 * ck_words(R) + tqq;
-        pf(wd + 32 * rqq);
-        if (rqq == 0) pf(wd + 32 * R);
-      }
-      if (t2 > 0) {
-        const int idx = 32 * w - t2 + lane + (t2 - 1);
-        pf(rowp(strip, ck_boundary(t2 - 1, CL)) + idx);
-      }
-    }
-    if (w > 0 && (t0 > 0 || strip > 0)) {
-      const uint2 *row = t0 > 0 ? rowp(strip, ck_boundary(t0 - 1, CL)) : rowp(strip - 1, CL.nb - 1);
-      const int idx = 32 * (w - 1) - t0 + lane + (t0 > 0 ? t0 - 1 : 31);
-      if (idx >= 0) pf(row + idx);
-    }
-  }
+  // (An L2 prefetch of the checkpoint lines of the tiles the walk can go to
+  // next -- left and up -- was 1-2 % slower on configs 2/3 in round 2.)
   // Column-parallel replay: lane l owns column c_lo(row) + l and the warp
   // steps down the tile one row at a time (no wavefront skew).  Per row:
   //   F  = max(F_up - ext, H_up - open)            (vertical, from the row above)
