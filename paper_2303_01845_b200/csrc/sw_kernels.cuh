@@ -906,6 +906,9 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t *codes, int R, int BPL
 // warp-uniform and compares loaded values exactly as the reference does.
 // ---------------------------------------------------------------------------
 constexpr int kTbWarps = 4;
+// residue bytes of a tile: read-only during K5 and reused by neighbouring
+// tiles, so through L1 (A/B against L1-bypassing loads: +0.5 % config 3)
+#define LD5 __ldg
 constexpr int16_t kNeg16 = -16384;  // boundary "-inf": below -open - ext for open <= 16383
 
 // Tile of class R: rows = G*R replayed + 1 halo, columns = G + 32 (halo +
@@ -958,9 +961,9 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   // latencies overlap, then the LUT lookups, then the shared-memory stores.
   const int c0 = cmin + lane, c1 = cmin + 32 + lane;
   const bool ok0 = (c0 >= 0) & (c0 < n), ok1 = (32 + lane < width) & (c1 >= 0) & (c1 < n);
-  const uint8_t rb0 = ok0 ? __ldcg(braw + c0) : (uint8_t)0;
-  const uint8_t rb1 = ok1 ? __ldcg(braw + c1) : (uint8_t)0;
-  const uint8_t ra = real_row ? __ldcg(araw + rho) : (uint8_t)0;
+  const uint8_t rb0 = ok0 ? LD5(braw + c0) : (uint8_t)0;
+  const uint8_t rb1 = ok1 ? LD5(braw + c1) : (uint8_t)0;
+  const uint8_t ra = real_row ? LD5(araw + rho) : (uint8_t)0;
   uint32_t ckx = 0u, cky = 0u;
   const bool have_ck = (w > 0) & row_ok;
   if (have_ck) {
