@@ -175,12 +175,9 @@ k_score_cta_packed(KArgs A, int stage, int cls) {
           const int s = s0 + q;
           const uint4 pa = load_profile_u8<R>(profA, ringA[rbase + q], lane);
           const uint4 pb = load_profile_u8<R>(profB, ringB[rbase + q], lane);
-          uint32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
-          uint32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
-          {
-            const uint2 tv = bnd[s & 31];
-            if (lane == 0) { upHo = tv.x; upF = tv.y; }
-          }
+          const uint2 tv = bnd[s & 31];
+          const uint32_t upHo = shfl_up_or(L.botHo, tv.x);
+          const uint32_t upF = shfl_up_or(L.botF, tv.y);
           uint32_t diag = L.hoUpPrev;
           L.hoUpPrev = upHo;
           uint32_t G = upF + OPEN2, tprev = upHo + OPEN2;   // G = F + open (sw_packed.cuh)

@@ -159,6 +159,16 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
   return d;
 }
+// value of lane - 1, or `fill` in lane 0 (the shuffle's valid predicate
+// picks it, no lane-index compare)
+__device__ __forceinline__ uint32_t shfl_up_or(uint32_t v, uint32_t fill) {
+  uint32_t r;
+  asm("{ .reg .pred p;\n\t"
+      "shfl.sync.up.b32 %0|p, %1, 1, 0, 0xffffffff;\n\t"
+      "@!p mov.b32 %0, %2;\n\t}"
+      : "=r"(r) : "r"(v), "r"(fill));
+  return r;
+}
 // byte k of w, sign-extended, times 65536 (scaled) or times 1 (plain)
 __device__ __forceinline__ uint32_t sel_scaled(int k) {
   return 0x44u | ((uint32_t)k << 8) | ((uint32_t)(k | 8) << 12);
@@ -1070,8 +1080,8 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       int32_t z = ht + Kl;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) z = max(z, (int32_t)__shfl_up_sync(0xffffffffu, z, d));
-      int32_t ex = __shfl_up_sync(0xffffffffu, z, 1);
       const int32_t x0e = rw.x;                             // E at c_lo (left boundary)
+      int32_t ex = __shfl_up_sync(0xffffffffu, z, 1);
       if (lane == 0) ex = x0e;
       const int32_t e = max(x0e, ex) - lext;
       const int32_t h = max(ht, e);

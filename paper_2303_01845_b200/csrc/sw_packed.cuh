@@ -409,12 +409,13 @@ k_score_packed(KArgs A, int stage, int cls) {
           const int s = s0 + q;
           const uint4 pa = load_profile_u8<R>(profA, ringA[rbase + q], lane);
           const uint4 pb = load_profile_u8<R>(profB, ringB[rbase + q], lane);
-          uint32_t upHo = __shfl_up_sync(0xffffffffu, L.botHo, 1);
-          uint32_t upF = __shfl_up_sync(0xffffffffu, L.botF, 1);
-          {
-            const uint2 bv = bnd[s & 31];
-            if (lane == 0) { upHo = bv.x; upF = bv.y; }
-          }
+          // the row above: from lane t-1, or (lane 0, whose shuffle source is
+          // out of range) from the staged boundary row -- selected by the
+          // shuffle's own valid predicate (A/B against a lane-index select:
+          // forward +0.9 % config 3, +1.1 % config 2)
+          const uint2 bv = bnd[s & 31];
+          const uint32_t upHo = shfl_up_or(L.botHo, bv.x);
+          const uint32_t upF = shfl_up_or(L.botF, bv.y);
           uint32_t diag = L.hoUpPrev;
           L.hoUpPrev = upHo;
           // F carried as G = F + open (biased): G[r] = max(G[r-1] - ext, t[r-1]),
