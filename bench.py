@@ -209,9 +209,9 @@ def packed_class_of(m: np.ndarray, n: np.ndarray) -> np.ndarray:
 
 def computed_cells(table) -> dict:
     """Cells K1p computes per algorithmic cell for this batch: each work list
-    (class) is sorted by shape (m, n descending) and consumed two pairs per
-    warp; a duo computes strips(max m) x 32R rows x (max n + 31) wavefront
-    steps in both u16 halves."""
+    (class) is sorted by strip count, then n (descending; k_classify) and
+    consumed two pairs per warp; a duo computes strips(max m) x 32R rows x
+    (max n + 31) wavefront steps in both u16 halves."""
     m = table["a_len"].astype(np.int64)
     n = table["b_len"].astype(np.int64)
     cells = m * n
@@ -220,7 +220,9 @@ def computed_cells(table) -> dict:
         return {"computed_cells_per_cell": None, "k1p_cell_fraction": 0.0}
     m, n = m[k1p], n[k1p]
     cls = packed_class_of(m, n)
-    order = np.lexsort((np.arange(len(m)), -n, -m, cls))
+    rows_of = np.asarray(CLASS_ROWS)[cls]
+    strips = (m + 32 * rows_of - 1) // (32 * rows_of)
+    order = np.lexsort((np.arange(len(m)), -n, -strips, cls))
     m, n, cls = m[order], n[order], cls[order]
     comp = 0
     for c, R in enumerate(CLASS_ROWS):
