@@ -119,6 +119,45 @@ def test_high_scores_above_int16_tiles_exact():
     assert rec["score"][4] == 35000 and rec["score"][2] == 32800
 
 
+def test_tie_heavy_pairs_exact():
+    """Row-major-first end cells and traceback priorities where ties are the
+    rule: a 4-letter alphabet under a +1/-1 matrix with gap 1/1, 20,000
+    random pairs of 100-900 residues across the packed classes, strips and
+    windows; plus 200 constructed pairs where the best score is reached at
+    (r, late column) and at (r + 1, early column): a = random, b = a[r-L+2 ..
+    r+1] + W-padding + a[r-L+1 .. r] (W matches nothing in a).  The lane
+    maxima in the checkpoints then point K5 at row r+1's early window, so row
+    r = i_end's j_end needs the later window's replay (~90 % of these pairs,
+    checked with a numpy DP when the test was written)."""
+    rng = np.random.default_rng(11)
+    alpha = np.frombuffer(b"ACGT", np.uint8)
+    sa, sb = [], []
+    wpad = np.frombuffer(b"W", np.uint8)
+    for k in range(200):
+        m = int(rng.integers(150, 800))
+        a = alpha[rng.integers(0, 4, m)]
+        L = int(rng.integers(30, 60))
+        r = int(rng.integers(L, m - 2))
+        b = np.concatenate([a[r - L + 2:r + 2], np.repeat(wpad, int(rng.integers(70, 300))),
+                            a[r - L + 1:r + 1], np.repeat(wpad, int(rng.integers(0, 50)))])
+        sa.append(a.tobytes())
+        sb.append(b.tobytes())
+    for k in range(20_000):
+        m, n = (int(x) for x in rng.integers(100, 900, 2))
+        a = alpha[rng.integers(0, 4, m)]
+        if k % 2:
+            b = alpha[rng.integers(0, 4, n)]
+        else:
+            b = a[rng.integers(0, max(1, m - n)) if m > n else 0:][:n].copy()
+            mut = rng.random(len(b)) < 0.2
+            b[mut] = alpha[rng.integers(0, 4, int(mut.sum()))]
+        sa.append(a.tobytes())
+        sb.append(b.tobytes())
+    from paper_2303_01845_b200.batch import pack_codes
+    arena, table = pack_codes(sa, sb)
+    _assert_exact(arena, table, 1, 1, _ident_matrix(1, -1))
+
+
 def test_unaligned_device_arena():
     """the device entry point takes arenas at any byte
     offset (k_encode handles the unaligned head)."""
