@@ -20,8 +20,9 @@
  *   address; every other item is left to phase B.
  * Phase B (calling thread, Python semantics): the remaining items, in input
  *   order, with the reference's exact checks and exceptions.
- * Then arena offsets are a prefix sum over the first uses in input order
- *   (deterministic layout; phase D rewrites the table's piece ids).
+ * Then arena offsets are a prefix sum over the pieces in input order (a
+ *   shared object's bytes sit at the piece of whichever of its users the
+ *   threads resolved first; phase D rewrites the table's piece ids).
  * Phase C: the arena buffer comes from the caller's alloc(nbytes) (pinned host
  *   memory from the engine's pool) and the distinct sequences are copied into
  *   it by the worker threads with the GIL released.
@@ -66,7 +67,7 @@ static inline size_t hash_ptr(uintptr_t p) {
 /* find or insert object `s`, whose bytes would become piece `pid`; returns
  * the piece id holding its bytes (== pid when this call inserted it).  No
  * shared counter: arena offsets are assigned afterwards by a prefix sum over
- * the pieces in input order, so the layout is deterministic. */
+ * the pieces in input order. */
 static uint64_t omap_get(omap_t *M, uintptr_t s, uint64_t pid) {
   size_t i = hash_ptr(s) & M->mask;
   for (;;) {

@@ -165,6 +165,50 @@ def test_pack_pairs_parallel_path_matches_sequential_semantics():
     assert len(raw) <= sum(len(s) for s in seqs) + 65001   # distinct objects stored once
 
 
+def test_pack_pairs_concurrent_calls_and_map_reuse():
+    """The packer keeps its dedup maps between calls (cleared after use) and
+    two batches may be packed at once (AlignEngine's two host threads): many
+    concurrent and repeated calls, with different sizes and sharing patterns,
+    each give a table whose every pair points at the same bytes as in a call
+    made alone (which user of a shared object owns its bytes is up to the
+    packing threads, so offsets may differ)."""
+    import threading
+    rng = np.random.default_rng(7)
+    seqs = ["".join(rng.choice(list("ACDEFGHIKLMNPQRSTVWY"), size=int(n)))
+            for n in rng.integers(1, 300, size=800)]
+
+    def batch_of(seed, n):
+        r = np.random.default_rng(seed)
+        return [(seqs[int(i)], seqs[int(j)], None) for i, j in r.integers(0, 800, size=(n, 2))]
+
+    jobs = [batch_of(s, n) for s, n in ((1, 9000), (2, 20000), (3, 500), (4, 13000))]
+    alone = [sw.pack_pairs(b) for b in jobs]
+
+    def check(b, ref):
+        got = sw.pack_pairs(b)
+        raw, rraw = bytes(got.arena), bytes(ref.arena)
+        assert len(got.pairs) == len(ref.pairs) and not got.errors
+        for (ao, bo, la, lb), (rao, rbo, _, _) in zip(got.pairs.tolist(), ref.pairs.tolist()):
+            assert raw[ao:ao + la] == rraw[rao:rao + la] and raw[bo:bo + lb] == rraw[rbo:rbo + lb]
+        assert len(raw) == len(rraw)              # each distinct object stored once
+
+    errors = []
+
+    def worker(k):
+        try:
+            for rep in range(3):
+                check(jobs[(k + rep) % 4], alone[(k + rep) % 4])
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[0]
+
+
 def test_result_list_is_lazy_and_list_like():
     from paper_2303_01845_b200 import _native
     from paper_2303_01845_b200.align import ResultList
