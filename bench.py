@@ -370,8 +370,9 @@ def main():
 
     def pinned(nbytes):
         ptr = lib.sw_host_alloc(nbytes)
-        if not ptr:
-            raise RuntimeError("sw_host_alloc failed")
+        if not ptr:   # no page-locked memory left (e.g. many ranks): pageable fallback
+            print(f"bench: sw_host_alloc({nbytes}) failed; pageable host memory", file=sys.stderr)
+            return None, np.empty(nbytes, dtype=np.uint8)
         return ptr, np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(ptr))
 
     pins = []
@@ -516,7 +517,8 @@ def main():
         if world > 1:
             torch.distributed.destroy_process_group()
         for p in pins:
-            lib.sw_host_free(p)
+            if p:
+                lib.sw_host_free(p)
         return
 
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -608,7 +610,8 @@ def main():
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
     for p in pins:
-        lib.sw_host_free(p)
+        if p:
+            lib.sw_host_free(p)
     if world > 1:
         torch.distributed.destroy_process_group()
 
