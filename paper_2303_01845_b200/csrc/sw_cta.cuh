@@ -26,9 +26,11 @@ struct CtaSync {               // per-CTA shared state
   volatile int cons[kCtaWarps];   // columns consumed from the link leaving warp w
   int64_t item;
   volatile int dead_strip;      // reverse pass: first strip whose bottom row carries no live path
+  volatile int stop_col[8];     // reverse pass: strip k's bottom row is dead from column stop_col[k & 7]
   unsigned long long red_fwd[kCtaWarps];
   int red_x[kCtaWarps], red_y[kCtaWarps], red_v[kCtaWarps];
 };
+static_assert(sizeof(CtaSync) <= 256, "CtaSync must fit the 256 B reserved in kSmemCta");
 
 template <int R, int MODE>
 __global__ void __launch_bounds__(kCtaWarps * 32)
@@ -112,7 +114,39 @@ k_score_cta(KArgs A, int stage, int cls) {
       int2 *ring_in = rings + in_link * kRing, *ring_out = rings + warp * kRing;
       int2 cur = dflt;
       const int steps = n + 31;
+      const int prod_base = prod_total, cons_base = cons_total;
+      // reset by lane 31, the lane that publishes S.prod, before any column is published
+      if (MODE == 1 && lane == 31) S.stop_col[strip & 7] = 0x7fffffff;
       for (int s = 0; s < steps; ++s) {
+        if constexpr (MODE == 1) {
+          // Horizontal stop: every path from the anchor into the columns right
+          // of the wavefront crosses it (a lane's cells, the diagonal feed
+          // hoUpPrev, the F leaving its bottom row) or enters from the row
+          // above right of lane 0.  Once all of those are dead by the dead-
+          // strip criterion (H <= 0, E/F <= ext - open; the row above dead
+          // from its producer's stop column on), no cell to the right can
+          // equal best (score_pair's argument, applied to a column cut), so
+          // the strip ends here; its bottom row is dead from column s - 31 on.
+          if ((s % kCtaChunk) == 0 && s > 0) {
+            bool live = (L.hoUpPrev > -OPEN) | (L.botF > -OPEN - nEXT);
+#pragma unroll
+            for (int r = 0; r < R; ++r) live |= __viaddmax_s32(L.E[r], nEXT, L.Ho[r]) > -OPEN;
+            const bool top_dead = !has_above || S.stop_col[(strip - 1) & 7] <= s;
+            if (__all_sync(0xffffffffu, !live && top_dead)) {
+              if (has_below) {
+                if (lane == 31) S.stop_col[strip & 7] = max(0, s - 31);
+                __threadfence_block();
+                prod_total = prod_base + n;
+                if (lane == 31) S.prod[warp] = prod_total;
+              }
+              if (has_above) {
+                cons_total = cons_base + n;
+                if (lane == 0) S.cons[in_link] = cons_total;
+              }
+              break;
+            }
+          }
+        }
         // ---- top input of lane 0 (column s): fetched 32 columns at a time
         if (has_above && (s % kCtaChunk) == 0) {
           const int need = min(s + kCtaChunk, n);
@@ -123,7 +157,9 @@ k_score_cta(KArgs A, int stage, int cls) {
             __syncwarp();
             const int c = s + lane;
             cur = dflt;
-            if (c < n) cur = in_wrap ? wrap[c] : ring_in[(cons_total + lane) & (kRing - 1)];
+            // columns past the producer's stop column were never written: dead
+            if (c < n && (MODE == 0 || c < S.stop_col[(strip - 1) & 7]))
+              cur = in_wrap ? wrap[c] : ring_in[(cons_total + lane) & (kRing - 1)];
             __syncwarp();
             cons_total = target;
             if (lane == 0) S.cons[in_link] = cons_total;

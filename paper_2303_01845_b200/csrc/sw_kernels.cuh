@@ -350,15 +350,17 @@ __device__ __forceinline__ void build_profile(uint8_t *prof, const int8_t *mat, 
 // 32-column register chunk (double-buffered, coalesced loads).
 struct BoundaryReader {
   int2 cur, nxt;
+  int lim;   // columns >= lim read as dflt (n, or the reverse pass's stop column of the row above)
   __device__ __forceinline__ void init(const int2 *bnd, int n, int lane, int2 dflt) {
+    lim = n;
     cur = lane < n ? bnd[lane] : dflt;
     nxt = 32 + lane < n ? bnd[32 + lane] : dflt;
   }
-  __device__ __forceinline__ int2 get(const int2 *bnd, int s, int n, int lane, int2 dflt) {
+  __device__ __forceinline__ int2 get(const int2 *bnd, int s, int, int lane, int2 dflt) {
     if ((s & 31) == 0 && s > 0) {
       cur = nxt;
       const int c = s + 32 + lane;
-      nxt = c < n ? bnd[c] : dflt;
+      nxt = c < lim ? bnd[c] : dflt;
     }
     int2 v;
     v.x = __shfl_sync(0xffffffffu, cur.x, s & 31);
@@ -516,6 +518,7 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
   const int32_t ANC = FLOOR - OPEN;              // -inf in (H - open) form
   ScoreOut res{0ull, 0, 0, 0};
   const int nstrips = (m + 32 * R - 1) / (32 * R);
+  int stop_above = n;   // MODE 1: the row above is dead from this column on (k_score_cta)
   for (int strip = 0; strip < nstrips; ++strip) {
     const int row0 = strip * 32 * R;
     __syncwarp();
@@ -538,9 +541,20 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
     BoundaryReader br;
     const int2 dflt = MODE == 1 ? make_int2(ANC, ANC) : make_int2(-OPEN, kNegInf);
     bool alive = false;   // MODE 1: does the strip's bottom row still carry a live path?
-    if (has_above) br.init(bnd, n, lane, dflt);
+    if (has_above) br.init(bnd, MODE == 1 ? min(n, stop_above) : n, lane, dflt);
     const int steps = n + 31;
+    int stop = n;
     for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
+      if constexpr (MODE == 1) {
+        // horizontal stop (see k_score_cta): the wavefront and the row above
+        // right of lane 0 are dead -> nothing right of it can equal best
+        if ((s0 & 31) == 0 && s0 > 0 && (!has_above || stop_above <= s0)) {
+          bool live = (L.hoUpPrev > -OPEN) | (L.botF > -OPEN - nEXT);
+#pragma unroll
+          for (int r = 0; r < R; ++r) live |= __viaddmax_s32(L.E[r], nEXT, L.Ho[r]) > -OPEN;
+          if (__all_sync(0xffffffffu, !live)) { stop = max(0, s0 - 31); break; }
+        }
+      }
 #pragma unroll 2
       for (int q = 0; q < kScoreUnroll; ++q) {
         score_step<R, MODE, WIDE>(L, prof, cols, s0 + q, n, lane, has_above, has_below, br, bnd,
@@ -573,6 +587,7 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
     }
     if constexpr (MODE == 1) {
       if (!__shfl_sync(0xffffffffu, (int)alive, 31)) break;   // no optimal path below
+      stop_above = stop;
     }
   }
   // warp reduction

@@ -489,3 +489,77 @@ def test_lookahead_loop_with_batches_in_flight():
             drain_one()
     assert max_inflight == capacity + 1
     assert hashlib.sha256(sw.canonical_bytes(lines)).hexdigest() == d["canonical_sha256"]
+
+
+_AA = np.frombuffer(b"ARNDCQEGHILKMFPSTWYV", dtype=np.uint8)
+
+
+def _gapped_motif_pairs(seed: int, count: int):
+    """Long pairs whose best local alignment is a motif split by a long gap
+    (40-200 residues inserted on one side) inside random flanks, plus pairs
+    holding two equal copies of a motif far apart: the anchored reverse pass
+    has to carry an open gap (E or F state) across many 32-column chunks and
+    strips, and ties spread the cells reaching best -- the cases the reverse
+    pass's dead-strip and horizontal stops must not cut short."""
+    rng = np.random.default_rng(seed)
+    rnd = lambda k: _AA[rng.integers(0, 20, k)]   # noqa: E731
+    sa, sb = [], []
+    for k in range(count):
+        motif = rnd(int(rng.integers(40, 120)))
+        cut = int(rng.integers(10, len(motif) - 10))
+        gap = rnd(int(rng.choice([40, 90, 200])))
+        fa, fb = int(rng.integers(200, 3000)), int(rng.integers(200, 3000))
+        left, right = motif[:cut], motif[cut:]
+        if k % 3 == 0:    # gap in a (rows): vertical gap through strips
+            a = np.concatenate([rnd(fa), left, gap, right, rnd(300)])
+            b = np.concatenate([rnd(fb), left, right, rnd(300)])
+        elif k % 3 == 1:  # gap in b (columns): horizontal gap across chunks
+            a = np.concatenate([rnd(fa), left, right, rnd(300)])
+            b = np.concatenate([rnd(fb), left, gap, right, rnd(300)])
+        else:             # two copies of the motif, far apart in both sequences
+            a = np.concatenate([rnd(fa), motif, rnd(700), motif, rnd(100)])
+            b = np.concatenate([rnd(fb), motif, rnd(1500), motif, rnd(100)])
+        sa.append(a.tobytes())
+        sb.append(b.tobytes())
+    return sa, sb
+
+
+@pytest.mark.parametrize("mode", ["default", "box"])
+def test_reverse_pass_across_long_gaps_exact(mode):
+    """Gapped and repeated motifs in long random pairs (up to ~3,600 x 3,600,
+    the warp and CTA reverse passes) under three gap settings; "box" sends
+    every pair through the anchored reverse pass."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+from conftest import FIELDS, matrix
+from test_gpu_parity import _gapped_motif_pairs
+from paper_2303_01845_b200 import _native
+from paper_2303_01845_b200.batch import pack_codes
+from oracle import oracle
+bad, n = 0, 0
+m = matrix("blosum62")
+for seed, (go, ge) in enumerate([(11, 1), (6, 2), (3, 1)]):
+    sa, sb = _gapped_motif_pairs(100 + seed, 90)
+    arena, table = pack_codes(sa, sb)
+    rec, _ = _native.align_host(arena, table, _native.make_params(go, ge, m))
+    ref = oracle.align_batch_c(arena, table, go, ge, m, threads=16)
+    got = np.stack([rec[f] for f in FIELDS], axis=1)
+    bad += int((got != ref[:, :7]).any(axis=1).sum())
+    n += len(table)
+print(json.dumps({"bad": bad, "n": n}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    if mode == "box":
+        env["PASTIS_SW_TRACEBACK"] = "box"
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["bad"] == 0 and res["n"] == 270, res
