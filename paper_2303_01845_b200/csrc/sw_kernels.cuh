@@ -943,11 +943,20 @@ struct TbSmem {
   static constexpr int G = 32 / R;
   static constexpr int kRows = G * R + 1;
   static constexpr int kX = (G + 32 + 1) / 2 * 2;
-  int16_t H[kRows][kX], E[kRows][kX], F[kRows][kX];  // row 0 / col 0 = halo
+  // per cell: H (bits 0-15, 0 <= H <= kTileMax) | (H == F) << 16 | (H == E) << 17.
+  // The walk needs E and F only to enter a gap state (H == F / H == E) and,
+  // inside a gap run, as entry value + k * ext (a run that has not closed
+  // extends: F(i-1) = F(i) + ext), so the gap matrices are not stored.
+  uint32_t H[kRows][kX];  // row 0 / col 0 = halo
   int4 row[32];         // per tile row: E at c_lo, H at c_lo - 1, matrix row, diag above / F_bot
   uint8_t bcode[kX], braw[kX];
   uint8_t acode[32], araw[32];
 };
+
+template <int R>
+__device__ __forceinline__ int32_t tH(const TbSmem<R> &T, int row, int col) {
+  return (int32_t)(T.H[row][col] & 0xFFFFu);
+}
 
 // checkpoint words hold two biased u16 values (v + B)
 __device__ __forceinline__ int32_t ulo(uint32_t x, int32_t B) { return (int32_t)(x & 0xFFFFu) - B; }
@@ -1034,8 +1043,8 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   // each forward lane, the diagonal above it (column c_lo - 1 of the row above)
   const int x0 = t1 - tq;                    // tile column of c_lo(q) - 1
   if (row_ok) {
-    T.H[q + 1][x0] = (int16_t)(Ho + OPEN);
-    if (rq == 0) T.H[q][x0] = (int16_t)(hoUpPrevT + OPEN);
+    T.H[q + 1][x0] = (uint32_t)(Ho + OPEN);
+    if (rq == 0) T.H[q][x0] = (uint32_t)(hoUpPrevT + OPEN);
   }
   // top halo row: H of the row above the tile at columns c_lo(t0) .. +31;
   // lane l also keeps (Ho, F) of column c_lo(t0) + l packed for row 0's feed
@@ -1046,7 +1055,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       tHo = (int32_t)(hi ? (z.x >> 16) : (z.x & 0xFFFFu)) - B;
       tF = (int32_t)(hi ? (z.y >> 16) : (z.y & 0xFFFFu)) - B;
     }
-    T.H[0][t1 - t0 + 1 + lane] = (int16_t)(tHo + OPEN);
+    T.H[0][t1 - t0 + 1 + lane] = (uint32_t)(tHo + OPEN);
     topv = ((uint32_t)tHo & 0xFFFFu) | ((uint32_t)tF << 16);
   }
   // (An L2 prefetch of the checkpoint lines of the tiles the walk can go to
@@ -1100,9 +1109,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       if (lane == 0) ex = x0e;
       const int32_t e = max(x0e, ex) - lext;
       const int32_t h = max(ht, e);
-      T.H[qq + 1][xs] = (int16_t)h;
-      T.E[qq + 1][xs] = (int16_t)e;
-      T.F[qq + 1][xs] = (int16_t)f;
+      T.H[qq + 1][xs] = (uint32_t)h | ((uint32_t)(h == f) << 16) | ((uint32_t)(h == e) << 17);
       upH = h;
       upF = f;
       prevHb = rw.y;
@@ -1160,12 +1167,13 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       const int q = i_end - trow0;
       tqmax = q;
       const int c = 32 * wstar - t + lane;
-      const bool hit = (c >= 0) && (c <= kap_hi) && ((int32_t)T.H[q + 1][c - tcmin + 1] >= best);
+      const bool hit = (c >= 0) && (c <= kap_hi) && (tH(T, q + 1, c - tcmin + 1) >= best);
       const uint32_t hm = __ballot_sync(0xffffffffu, hit);
       if (hm) { j_end = 32 * wstar - t + __ffs(hm) - 1; break; }
     }
   }
   int i = i_end + 1, j = j_end + 1, state = 0, matches = 0, aln = 0;
+  int32_t gap = 0;   // state 1/2: F/E of the current cell
   bool lost = j_end < 0;
   for (;;) {
     if (lost) break;
@@ -1200,9 +1208,9 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       ok = ok && (xx >= tspan - qq / R + 1);
       bool dg = false, mt = false;
       if (ok) {
-        const int32_t hk = T.H[qq + 1][xx];
+        const int32_t hk = tH(T, qq + 1, xx);
         const int32_t sk = smat[T.acode[qq] * kCodes + T.bcode[xx - 1]];
-        dg = (hk != 0) && (hk == (int32_t)T.H[qq][xx - 1] + sk);
+        dg = (hk != 0) && (hk == tH(T, qq, xx - 1) + sk);
         mt = T.araw[qq] == T.braw[xx - 1];
       }
       const uint32_t run_mask = __ballot_sync(0xffffffffu, dg);
@@ -1214,11 +1222,13 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
         aln += run; i -= run; j -= run;
         continue;
       }
-      const int32_t h = T.H[q + 1][x];
+      const uint32_t hw = T.H[q + 1][x];
+      const int32_t h = (int32_t)(hw & 0xFFFFu);
       if (h == 0) break;
-      if (h == (int32_t)T.F[q + 1][x]) {
+      gap = h;                              // the gap state's value at this cell
+      if (hw & (1u << 16)) {
         state = 1;
-      } else if (h == (int32_t)T.E[q + 1][x]) {
+      } else if (hw & (1u << 17)) {
         state = 2;
       } else {
         lost = true;
@@ -1227,26 +1237,26 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
     } else if (state == 1) {                // align.py:152-160: vertical gap run
       const int qq = q - lane;
       const bool ok = (qq >= 0) && (x >= tspan - qq / R + 1);
-      const bool close =
-          ok && ((int32_t)T.F[qq + 1][x] == (int32_t)T.H[qq][x] - OPEN);
+      const bool close = ok && (gap + lane * EXT == tH(T, qq, x) - OPEN);   // F(qq) == H above - open
       const uint32_t cm = __ballot_sync(0xffffffffu, close);
       const uint32_t vm = __ballot_sync(0xffffffffu, ok);
       const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
       int steps;
       if (cm) { steps = __ffs(cm); state = 0; }
       else steps = nvalid;
+      gap += steps * EXT;
       aln += steps; i -= steps;
     } else {                                // align.py:161-169: horizontal gap run
       const int xx = x - lane;
       const bool ok = (kap - lane >= 0) && (xx >= tspan - q / R + 1);
-      const bool close =
-          ok && ((int32_t)T.E[q + 1][xx] == (int32_t)T.H[q + 1][xx - 1] - OPEN);
+      const bool close = ok && (gap + lane * EXT == tH(T, q + 1, xx - 1) - OPEN);   // E(xx) == H left - open
       const uint32_t cm = __ballot_sync(0xffffffffu, close);
       const uint32_t vm = __ballot_sync(0xffffffffu, ok);
       const int nvalid = __ffs(~vm) == 0 ? 32 : __ffs(~vm) - 1;
       int steps;
       if (cm) { steps = __ffs(cm); state = 0; }
       else steps = nvalid;
+      gap += steps * EXT;
       aln += steps; j -= steps;
     }
   }
@@ -1263,11 +1273,17 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
   }
 }
 
-template <int R>
-#ifndef K5_MINB9
-#define K5_MINB9 7
+// 9 blocks of 4 warps per SM (56 registers, no spills): the replay is latency
+// bound, and the u32 tile (no E/F matrices) leaves shared memory for 9 blocks
+// at R <= 9.  A/B on B200, config 3 / config 2 full GCUPS: 7 blocks (72
+// registers, 3 int16 tiles) 2,447 / 1,850; u32 tile at 7 blocks 2,446 / 1,840;
+// 8 blocks 2,531 / 1,892; 9 blocks 2,552 / 1,918; 10 blocks (48 registers,
+// spills) 2,493 / 1,892.
+#ifndef K5_MIN_BLOCKS
+#define K5_MIN_BLOCKS 9
 #endif
-__global__ void __launch_bounds__(kTbWarps * 32, (R == 9 ? K5_MINB9 : R >= 8 ? 7 : 6))
+template <int R>
+__global__ void __launch_bounds__(kTbWarps * 32, K5_MIN_BLOCKS)
 k_tb(KArgs A, int stage, int cls) {
   struct Shared {
     TbSmem<R> t[kTbWarps];
