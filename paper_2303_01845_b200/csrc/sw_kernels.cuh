@@ -943,10 +943,11 @@ struct TbSmem {
   static constexpr int G = 32 / R;
   static constexpr int kRows = G * R + 1;
   static constexpr int kX = (G + 32 + 1) / 2 * 2;
-  // per cell: H (bits 0-15, 0 <= H <= kTileMax) | (H == F) << 16 | (H == E) << 17.
-  // The walk needs E and F only to enter a gap state (H == F / H == E) and,
-  // inside a gap run, as entry value + k * ext (a run that has not closed
-  // extends: F(i-1) = F(i) + ext), so the gap matrices are not stored.
+  // per cell: H (bits 0-15, 0 <= H <= kTileMax) | (F + open) << 16 (-open <= F <= H).
+  // The walk needs F and E only to enter a gap state and, inside a gap run,
+  // as entry value + k * ext (a run that has not closed extends: F(i-1) =
+  // F(i) + ext); a cell that is neither a diagonal move nor H == F has H == E
+  // (H = max(D, E, F, 0)), so E is not stored at all.
   uint32_t H[kRows][kX];  // row 0 / col 0 = halo
   int4 row[32];         // per tile row: E at c_lo, H at c_lo - 1, matrix row, diag above / F_bot
   uint8_t bcode[kX], braw[kX];
@@ -1109,7 +1110,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       if (lane == 0) ex = x0e;
       const int32_t e = max(x0e, ex) - lext;
       const int32_t h = max(ht, e);
-      T.H[qq + 1][xs] = (uint32_t)h | ((uint32_t)(h == f) << 16) | ((uint32_t)(h == e) << 17);
+      T.H[qq + 1][xs] = (uint32_t)(h + (OPEN << 16)) + ((uint32_t)f << 16);   // h | (f + open) << 16
       upH = h;
       upF = f;
       prevHb = rw.y;
@@ -1226,14 +1227,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       const int32_t h = (int32_t)(hw & 0xFFFFu);
       if (h == 0) break;
       gap = h;                              // the gap state's value at this cell
-      if (hw & (1u << 16)) {
-        state = 1;
-      } else if (hw & (1u << 17)) {
-        state = 2;
-      } else {
-        lost = true;
-        break;
-      }
+      state = h == (int32_t)(hw >> 16) - OPEN ? 1 : 2;   // F first (align.py:145-150), else E
     } else if (state == 1) {                // align.py:152-160: vertical gap run
       const int qq = q - lane;
       const bool ok = (qq >= 0) && (x >= tspan - qq / R + 1);
