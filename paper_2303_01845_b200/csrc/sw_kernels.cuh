@@ -1092,9 +1092,7 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
     const int xs = (t1 - tb) + 1 + lane;    // tile column of this lane's cell
     const int8_t *mcol = smat + T.bcode[xs - 1];
     const int nr = min(R, qmax + 1 - qs);   // rows of this forward lane to replay
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (r >= nr) break;
+    auto row_step = [&](const int r) {
       const int qq = qs + r;
       const int4 rw = T.row[qq];             // broadcast
       int32_t dg = __shfl_up_sync(0xffffffffu, upH, 1);
@@ -1115,6 +1113,16 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
       upF = f;
       prevHb = rw.y;
       prevFb = rw.w;                         // used after the forward lane's last row
+    };
+    if (nr == R) {                           // whole forward lane: no per-row exit test
+#pragma unroll
+      for (int r = 0; r < R; ++r) row_step(r);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r >= nr) break;
+        row_step(r);
+      }
     }
   }
   __syncwarp();
