@@ -327,7 +327,7 @@ k_jend(KArgs A, int stage, int cls) {
     __syncwarp();
     const View rows{A.codes + p.a_off + row0, 1}, cols{A.codes + p.b_off, 1};
     const ScoreOut o = score_pair<R, 0, true>(prof, smat, rows, cols, i_end - row0 + 1, n, A.open_,
-                                              A.ext, 0, bnd, lane, strip > 0);
+                                              A.ext, best, bnd, lane, strip > 0);   // stops at best
     if (lane == 0) {
       const int32_t j_end = 65535 - (int32_t)(o.fwd & 0xFFFF);
       const int32_t got = (int32_t)(o.fwd >> 32);

@@ -545,6 +545,21 @@ __device__ __forceinline__ ScoreOut score_pair(uint8_t *prof, const int8_t *mat,
     const int steps = n + 31;
     int stop = n;
     for (int s0 = 0; s0 < steps; s0 += kScoreUnroll) {
+      if constexpr (MODE == 0) {
+        // k_jend (best_known = the pair's best, rows up to i_end): every row
+        // above i_end stays below best, so the first cell reaching best is
+        // (i_end, j_end) and later columns cannot change the row-major-first
+        // argmax -- stop there
+        if (best_known > 0 && (s0 & 31) == 0 && s0 > 0) {
+          bool hit = false;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if constexpr (WIDE) hit |= (int32_t)(L.key[r] >> 32) >= best_known;
+            else hit |= (L.key[r] >> 16) >= best_known;
+          }
+          if (__any_sync(0xffffffffu, hit)) break;
+        }
+      }
       if constexpr (MODE == 1) {
         // horizontal stop (see k_score_cta): the wavefront and the row above
         // right of lane 0 are dead -> nothing right of it can equal best
