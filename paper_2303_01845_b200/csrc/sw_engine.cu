@@ -1173,6 +1173,13 @@ int sw_get_device_count(void) {
 }
 
 const char *sw_last_error(void) { return g_err.c_str(); }
+#ifdef K5_COUNT
+int sw_debug_k5_counters(unsigned long long *out) {   // debug builds only
+  cudaMemcpyFromSymbol(out, pastis::g_k5c, sizeof(unsigned long long) * 8);
+  static const unsigned long long zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  return (int)cudaMemcpyToSymbol(pastis::g_k5c, zero, sizeof(zero));
+}
+#endif
 
 int sw_align_batch(int device, const uint8_t *arena, uint64_t arena_bytes, const sw_pair_t *pairs,
                    uint64_t n_pairs, const sw_params_t *params, sw_result_t *out,

@@ -1143,6 +1143,12 @@ __device__ __forceinline__ void tb_replay(TbSmem<R> &T, const int8_t *smat, cons
   __syncwarp();
 }
 
+#ifdef K5_COUNT
+__device__ unsigned long long g_k5c[8];   // debug: pairs, j tiles, j rows, walk tiles, walk rows, aln, iters
+#define K5C(i, v) do { if (lane == 0) atomicAdd(&g_k5c[i], (unsigned long long)(v)); } while (0)
+#else
+#define K5C(i, v) do { } while (0)
+#endif
 // Traceback of one pair whose packed forward pass wrote checkpoints
 // (PairState: best, i_end, code_off, box_n, flags & kFlagNeedJ); one warp.
 template <int R>
@@ -1187,6 +1193,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       if (32 * wstar - t > kap_hi) continue;
       tb_replay<R>(T, smat, slut, ck, rowck, hi, CL, strip, g, wstar, m, n, acodes, bcodes, araw, braw, lane, OPEN,
                    EXT, Bias, trow0, tcmin, i_end, kap_hi);
+      K5C(1, 1); K5C(2, i_end - trow0 + 1);
       cs = strip; cg = g; cw = wstar;
       const int q = i_end - trow0;
       tqmax = q;
@@ -1216,6 +1223,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       const int w = (kap + t) >> 5;
       tb_replay<R>(T, smat, slut, ck, rowck, hi, CL, strip, g, w, m, n, acodes, bcodes, araw, braw, lane, OPEN,
                    EXT, Bias, trow0, tcmin, rho, kap);
+      K5C(3, 1); K5C(4, rho - trow0 + 1);
       cs = strip; cg = g; cw = w;
       q = rho - trow0;
       tqmax = q;
@@ -1277,6 +1285,7 @@ __device__ __forceinline__ void tb_pair(const KArgs &A, TbSmem<R> &T, const int8
       aln += steps; j -= steps;
     }
   }
+  K5C(0, 1); K5C(5, aln);
   if (lane == 0) {
     sw_result_t r;
     r.score = st->best;
