@@ -45,7 +45,10 @@ __host__ __device__ constexpr int smem_cta_packed(int R) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(kCtaWarps * 32, 3)
+#ifndef K1CP_MINB
+#define K1CP_MINB 3
+#endif
+__global__ void __launch_bounds__(kCtaWarps * 32, K1CP_MINB)
 k_score_cta_packed(KArgs A, int stage, int cls) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t *smatT = smem;
