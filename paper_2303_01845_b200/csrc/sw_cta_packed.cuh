@@ -46,7 +46,7 @@ __host__ __device__ constexpr int smem_cta_packed(int R) {
 
 template <int R>
 #ifndef K1CP_MINB
-#define K1CP_MINB 3
+#define K1CP_MINB 4   // 126 registers, 4 blocks of 4 warps (config 5 forward +0.6 % over 3 blocks at 166)
 #endif
 __global__ void __launch_bounds__(kCtaWarps * 32, K1CP_MINB)
 k_score_cta_packed(KArgs A, int stage, int cls) {
