@@ -54,7 +54,7 @@ class PackedBatch:
     @property
     def cells(self) -> int:
         p = self.pairs
-        return int(np.dot(p["a_len"].astype(np.uint64), p["b_len"].astype(np.uint64)))
+        return int((p["a_len"].astype(np.uint64) * p["b_len"]).sum())   # no BLAS, exact
 
 
 def _numpy_alloc(nbytes: int) -> np.ndarray:
