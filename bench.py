@@ -642,13 +642,42 @@ def api_leg(args, arena_np, table_np, cells, flush, torch) -> dict:
         if step >= warm:
             walls.append(dt)
             phases.append(getattr(eng, "last_phases", {}))
-    eng.close()
     assert not errors and len(results) == len(pairs)
+    del results, errors, counters, lanes
+    # pipelined: batch k+1 submitted before batch k's result is taken (the
+    # reference pipeline's lookahead, pipeline.py:209-212), so its packing
+    # runs beside batch k's GPU work on the engine's second host thread
+    # (one untimed pipelined round first: two batches in flight need a second
+    # pinned arena in the engine's pool, a one-time cudaHostAlloc of ~0.4 s)
+    def pipelined(nb):
+        done = []
+        pend = eng.submit(pairs)
+        for k in range(nb):
+            nxt = eng.submit(pairs) if k + 1 < nb else None
+            res = pend.result()
+            done.append(time.perf_counter())
+            assert not res[1] and len(res[0]) == len(pairs)
+            del res
+            pend = nxt
+        return done
+    pipelined(4)
+    torch.cuda.synchronize()
+    nb = 8
+    done = pipelined(nb)
+    # steady state: batches completed per second after the first completion
+    piped = (done[-1] - done[0]) / (nb - 1)
+    gaps = [round((b - a) * 1e3, 1) for a, b in zip(done, done[1:])]
+    eng.close()
     wall = float(np.mean(walls))
     out = {"value": cells / wall / 1e9, "unit": "GCUPS", "ms_per_step": wall * 1e3,
            "alignments_per_sec": len(pairs) / wall,
            "entry": "AlignEngine(lanes=1, use_processes=True).submit(list[(str, str, None)])"
-                    ".result()"}
+                    ".result()",
+           "pipelined": {"value": cells / piped / 1e9, "unit": "GCUPS", "ms_per_batch": piped * 1e3,
+                         "batches": nb, "in_flight": 2, "completion_gaps_ms": gaps,
+                         "median_gap_ms": float(np.median(gaps)),
+                         "note": "submit(batch k+1) before result(batch k): packing overlaps "
+                                 "the previous batch's GPU work"}}
     if phases and phases[0]:
         out["phase_ms"] = {k: float(np.mean([p[k] for p in phases])) * 1e3 for k in phases[0]
                            if k != "chunks"}

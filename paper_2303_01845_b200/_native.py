@@ -325,7 +325,7 @@ class PinnedPool:
     GPU read the arena directly (zero-copy) on the multi-GPU path.  When no
     CUDA driver is present (CPU tests) it hands out plain numpy memory."""
 
-    def __init__(self, max_free: int = 4):
+    def __init__(self, max_free: int = 8):
         self._free: list = []
         self._lock = threading.Lock()
         self._max_free = max_free

@@ -133,3 +133,34 @@ if "--chunk" in sys.argv:
         ph = eng.last_phases
         print(f"chunk {ch}: calls ms {[round(t, 1) for t in ts[2:]]} last phases "
               f"{ {k: round(v * 1e3, 1) for k, v in ph.items() if k != 'chunks'} } chunks {ph['chunks']}")
+
+if "--piped" in sys.argv:
+    import paper_2303_01845_b200 as sw
+    from paper_2303_01845_b200 import _native
+    pool = _native.pinned_pool()
+    orig = pool.acquire
+
+    def acquire(nbytes):
+        n_free = len(pool._free)
+        t0 = time.perf_counter()
+        b = orig(nbytes)
+        dt = (time.perf_counter() - t0) * 1e3
+        if dt > 1:
+            print(f"  acquire {nbytes / 2**20:.0f} MiB took {dt:.1f} ms (free list {n_free})")
+        return b
+    pool.acquire = acquire
+    eng = sw.AlignEngine(sw.AlignParams(gap_open=11, gap_extend=1), lanes=1, use_processes=True)
+    eng.start()
+    for rep in range(2):
+        eng.submit(pairs).result()
+    print("pipelined")
+    t0 = time.perf_counter()
+    pend = eng.submit(pairs)
+    for k in range(4):
+        nxt = eng.submit(pairs) if k + 1 < 4 else None
+        res = pend.result()
+        print(f"batch {k} done at {(time.perf_counter() - t0) * 1e3:.1f} ms phases "
+              f"{ {a: round(v * 1e3, 1) for a, v in eng.last_phases.items() if a != 'chunks'} }")
+        del res
+        pend = nxt
+    eng.close()
