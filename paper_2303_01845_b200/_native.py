@@ -325,10 +325,13 @@ class PinnedPool:
     GPU read the arena directly (zero-copy) on the multi-GPU path.  When no
     CUDA driver is present (CPU tests) it hands out plain numpy memory."""
 
-    def __init__(self, max_free: int = 8):
+    def __init__(self, max_free: int = 8, max_free_bytes: int = 3 << 30):
+        # up to 8 buffers / 3 GiB kept free: two batches in flight through the
+        # engine (arena, table and records each) without a cudaHostAlloc per call
         self._free: list = []
         self._lock = threading.Lock()
         self._max_free = max_free
+        self._max_free_bytes = max_free_bytes
 
     def acquire(self, nbytes: int):
         nbytes = max(int(nbytes), 1)
@@ -350,6 +353,10 @@ class PinnedPool:
             self._free.append((ptr, cap))
             while len(self._free) > self._max_free:
                 p, _ = min(self._free, key=lambda b: b[1])
+                self._free.remove((p, _))
+                load().sw_host_free(p)
+            while len(self._free) > 1 and sum(c for _, c in self._free) > self._max_free_bytes:
+                p, _ = max(self._free, key=lambda b: b[1])
                 self._free.remove((p, _))
                 load().sw_host_free(p)
 
