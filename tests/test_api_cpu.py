@@ -280,3 +280,53 @@ def test_chunked_pipeline_merges_like_one_batch(monkeypatch):
     assert one[2].alignments == many[2].alignments and one[2].cells == many[2].cells
     assert list(one[0]) == list(many[0])
     assert many[0][41] is None and many[0][3].cells == len(seqs[3]) * len(seqs[10])
+
+
+def test_pinned_pool_reuse_and_caps(monkeypatch):
+    """PinnedPool hands back the smallest free buffer that fits, keeps at most
+    max_free buffers (smallest freed first) and max_free_bytes (largest freed
+    first), against a fake allocator (no CUDA driver here)."""
+    import ctypes
+    from paper_2303_01845_b200 import _native
+
+    class FakeLib:
+        def __init__(self):
+            self.live, self.allocs, self.frees = {}, 0, 0
+
+        def sw_host_alloc(self, n):
+            buf = ctypes.create_string_buffer(n)
+            ptr = ctypes.addressof(buf)
+            self.live[ptr] = buf
+            self.allocs += 1
+            return ptr
+
+        def sw_host_free(self, ptr):
+            del self.live[ptr]
+            self.frees += 1
+
+    fake = FakeLib()
+    monkeypatch.setattr(_native, "load", lambda *a, **k: fake)
+    pool = _native.PinnedPool(max_free=3, max_free_bytes=5 << 20)
+    a = pool.acquire(3 << 20)            # 4 MiB cap
+    b = pool.acquire(100)                # 1 MiB cap
+    assert a.pinned and b.pinned and a.cap == 4 << 20 and b.cap == 1 << 20
+    a.array[:] = 7
+    a.release(); b.release()
+    assert fake.allocs == 2 and fake.frees == 0
+    c = pool.acquire(10)                 # smallest fit: the 1 MiB buffer
+    assert c.cap == 1 << 20 and fake.allocs == 2
+    c.release()
+    bufs = [pool.acquire(1 << 20) for _ in range(4)]   # the 1 MiB, the 4 MiB, 2 new
+    assert fake.allocs == 4 and sorted(x.cap for x in bufs) == [1 << 20] * 3 + [4 << 20]
+    for x in bufs:
+        x.release()
+    # released one by one: with 1 + 4 + 1 MiB free (6 MiB > 5 MiB) the largest
+    # goes; the last 1 MiB then fits both caps
+    caps = sorted(cap for _, cap in pool._free)
+    assert caps == [1 << 20] * 3
+    assert fake.frees == 1 and len(fake.live) == 3
+    extra = [pool.acquire(1 << 20) for _ in range(4)]   # 3 reused + 1 new
+    assert fake.allocs == 5
+    for x in extra:
+        x.release()
+    assert len(pool._free) == 3 and fake.frees == 2      # count cap: one 1 MiB freed
