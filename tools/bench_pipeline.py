@@ -4,7 +4,10 @@ stage (RunStats) after one warm-up run, with the canonical digest checked
 against the reference's (a841c454...).  The reference's own
 run of the same config took 935 s on 8 cores.
 
-    python tools/bench_pipeline.py [count seed] [--cpu-baseline]
+    python tools/bench_pipeline.py [count seed] [--cpu-baseline] [--gpus N]
+
+--gpus N runs the GPU stages on devices 0..N-1 (default: every visible GPU,
+PipelineConfig.devices = None).
 
 --cpu-baseline also times the reference ALGORITHM's alignment stage on the
 box's host cores over exactly the pipeline's SW pairs (the numpy
@@ -50,23 +53,31 @@ def cpu_align_baseline(fa_path, td):
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    argv = sys.argv[1:]
+    devices = None
+    if "--gpus" in argv:
+        k = argv.index("--gpus")
+        devices = tuple(range(int(argv[k + 1])))
+        del argv[k:k + 2]
+    args = [a for a in argv if not a.startswith("--")]
     count = int(args[0]) if len(args) > 0 else 100_000
     seed = int(args[1]) if len(args) > 1 else 4
+    cfg = pipeline.PipelineConfig(devices=devices)
     with tempfile.TemporaryDirectory() as td:
         fa = os.path.join(td, "in.fa")
         t0 = time.perf_counter()
         corpus.write_fasta(fa, corpus.synthetic_records(count, seed))
         gen_s = time.perf_counter() - t0
         out = os.path.join(td, "out.tsv")
-        pipeline.run_search(pipeline.PipelineConfig(), fa, out)        # warm-up
+        pipeline.run_search(cfg, fa, out)        # warm-up
         runs = []
         for _ in range(3):
-            st = pipeline.run_search(pipeline.PipelineConfig(), fa, out)
+            st = pipeline.run_search(cfg, fa, out)
             runs.append(st.to_json())
         best = min(runs, key=lambda r: r["total_seconds"])
         best["digest"] = pipeline.canonical_digest(out)
         best["digest_matches_reference"] = best["digest"] == REF_DIGEST.get((count, seed))
+        best["gpus"] = len(devices) if devices else "all visible"
         best["corpus"] = {"count": count, "seed": seed, "generate_s": gen_s,
                           "fasta_mb": os.path.getsize(fa) / 1e6}
         if "--cpu-baseline" in sys.argv:
